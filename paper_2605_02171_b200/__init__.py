@@ -1,0 +1,316 @@
+"""B200-native BQ query path for QuIVer (`qivr`) — host-side mirror of the
+reference's index/search interface over the qvg C-ABI (include/qvg.h).
+
+Reference interface mirrored (paths under /root/reference/proj/core):
+  SearchParams / validate        search.hpp:12-20
+  SearchResult                   search.hpp:22-26
+  query(index, vec, params)      search.hpp:95-98, search.cpp:122-143
+  run_query_batch(index, q, nq, params, threads)   eval.hpp:42-44, eval.cpp:225-247
+  load_index / save_index        store_io.hpp:34-40
+  build_index                    builder.hpp:29-30 (GPU builder, qvg_build)
+Errors follow the reference's classes: InvalidArgument is a ValueError
+(std::invalid_argument), QvgRuntimeError a RuntimeError (std::runtime_error).
+
+Every compute call runs the sm_100a kernels in libqvg.so; importing this
+package fails if the library has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+from ._native import SENTINEL
+
+__all__ = [
+    "SearchParams", "SearchResult", "GpuIndex", "BuildParams", "query", "run_query_batch",
+    "encode_queries", "QvgError", "InvalidArgument", "QvgRuntimeError", "CudaError",
+    "OutOfMemory", "CapacityOverflow", "NotImplementedByQvg", "words_for_dim", "SENTINEL",
+]
+
+N.lib()  # fail loudly at import when the CUDA library is missing
+
+
+class QvgError(Exception):
+    status = -1
+
+
+class InvalidArgument(QvgError, ValueError):
+    status = N.QVG_INVALID_ARGUMENT
+
+
+class QvgRuntimeError(QvgError, RuntimeError):
+    status = N.QVG_RUNTIME_ERROR
+
+
+class CudaError(QvgError, RuntimeError):
+    status = N.QVG_CUDA_ERROR
+
+
+class OutOfMemory(QvgError, MemoryError):
+    status = N.QVG_OUT_OF_MEMORY
+
+
+class CapacityOverflow(QvgError, RuntimeError):
+    status = N.QVG_CAPACITY_OVERFLOW
+
+
+class NotImplementedByQvg(QvgError, NotImplementedError):
+    status = N.QVG_NOT_IMPLEMENTED
+
+
+_ERRORS = {c.status: c for c in (InvalidArgument, QvgRuntimeError, CudaError, OutOfMemory,
+                                 CapacityOverflow, NotImplementedByQvg)}
+
+
+def _check(rc: int):
+    if rc != N.QVG_OK:
+        raise _ERRORS.get(rc, QvgError)(N.last_error())
+
+
+def words_for_dim(dim: int) -> int:
+    """encoding.hpp:15"""
+    return (dim + 63) // 64
+
+
+@dataclass
+class SearchParams:
+    """search.hpp:12-20"""
+    ef: int = 64
+    k: int = 10
+
+    def validate(self):
+        if self.k < 1:
+            raise InvalidArgument("SearchParams: k must be >= 1")
+        if self.ef < self.k:
+            raise InvalidArgument("SearchParams: ef must be >= k")
+
+
+@dataclass
+class SearchResult:
+    """search.hpp:22-26 — top-k ids with cosine scores, descending, ties by id."""
+    ids: np.ndarray = field(default_factory=lambda: np.empty(0, np.uint32))
+    scores: np.ndarray = field(default_factory=lambda: np.empty(0, np.float32))
+
+
+@dataclass
+class BuildParams:
+    """graph.hpp:32-47 (+ GPU batching knobs)."""
+    m: int = 32
+    ef_c: int = 128
+    alpha: float = 1.2
+    passes: int = 1
+    batch: int = 0
+    seed: int = 42
+
+
+def _f32(a, cols=None):
+    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+        return a  # torch tensor: used as is (host or device)
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if cols is not None:
+        a = a.reshape(-1, cols)
+    return a
+
+
+class GpuIndex:
+    """An HBM-resident index (qvg_index handle)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        n, dim, R, entry = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(N.lib().qvg_index_info(self._h, C.byref(n), C.byref(dim), C.byref(R),
+                                      C.byref(entry)))
+        self.n, self.dim, self.max_degree, self.entry_point = (n.value, dim.value, R.value,
+                                                               entry.value)
+        self.W = words_for_dim(self.dim)
+
+    # ---- construction ---------------------------------------------------------
+    @classmethod
+    def from_arrays(cls, codes, adjacency, cold, entry_point, device=0):
+        """From the reference's raw layouts: codes n x 2W u64 (SignatureStore),
+        adjacency n x (R+1) u32 (AdjacencyTable slots), cold n x dim f32."""
+        codes = np.ascontiguousarray(codes, dtype=np.uint64)
+        adjacency = np.ascontiguousarray(adjacency, dtype=np.uint32)
+        cold = _f32(cold)
+        n, dim = cold.shape
+        if codes.shape != (n, 2 * words_for_dim(dim)):
+            raise InvalidArgument("codes shape does not match cold store")
+        if adjacency.ndim != 2 or adjacency.shape[0] != n:
+            raise InvalidArgument("adjacency shape does not match cold store")
+        h = C.c_void_p()
+        _check(N.lib().qvg_index_create(codes.ctypes.data, n, dim, adjacency.ctypes.data,
+                                        adjacency.shape[1] - 1, N.ptr(cold), int(entry_point),
+                                        device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, path, device=0):
+        """qivr::load_index for .qivr v1 files, straight into HBM."""
+        h = C.c_void_p()
+        _check(N.lib().qvg_index_load(str(path).encode(), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def build(cls, data, params: Optional[BuildParams] = None, device=0, stats=None):
+        """qivr::build_index on the GPU (batched BQ-space Vamana insertion)."""
+        p = params or BuildParams()
+        data = _f32(data)
+        n, dim = data.shape
+        bp = N.qvg_build_params(m=p.m, ef_c=p.ef_c, alpha=p.alpha, passes=p.passes,
+                                batch=p.batch, seed=p.seed)
+        bs = N.qvg_build_stats()
+        h = C.c_void_p()
+        _check(N.lib().qvg_build(N.ptr(data), n, dim, C.byref(bp), device, C.byref(h),
+                                 C.byref(bs)))
+        if stats is not None:
+            stats.update({f: getattr(bs, f) for f, _ in bs._fields_})
+        return cls(h)
+
+    def save(self, path):
+        _check(N.lib().qvg_index_save(self._h, str(path).encode()))
+
+    def export(self):
+        codes = np.empty((self.n, 2 * self.W), np.uint64)
+        adj = np.empty((self.n, self.max_degree + 1), np.uint32)
+        cold = np.empty((self.n, self.dim), np.float32)
+        _check(N.lib().qvg_index_export(self._h, codes.ctypes.data, adj.ctypes.data,
+                                        cold.ctypes.data))
+        return codes, adj, cold
+
+    def set_stream(self, stream):
+        """Issue all work on a caller stream (torch.cuda.Stream, int handle, or None)."""
+        if stream is None:
+            v = None
+        elif hasattr(stream, "cuda_stream"):
+            v = stream.cuda_stream
+        else:
+            v = int(stream)
+        _check(N.lib().qvg_index_set_stream(self._h, C.c_void_p(v) if v else None))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().qvg_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- search ------------------------------------------------------------------
+    def search(self, queries, k=10, ef=64, out=None, stats=False):
+        """Batched query -> (ids[nq,k] u32, scores[nq,k] f32, counts[nq] u32).
+        Rows past counts[i] hold SENTINEL / NaN.  `queries` may be a host numpy
+        array or a torch tensor (host or CUDA); `out` may supply (ids, scores,
+        counts) buffers (numpy or CUDA tensors)."""
+        q = _f32(queries, self.dim)
+        nq = q.shape[0] if isinstance(q, np.ndarray) else q.numel() // self.dim
+        if out is None:
+            ids = np.empty((nq, k), np.uint32)
+            sc = np.empty((nq, k), np.float32)
+            cnt = np.empty(nq, np.uint32)
+        else:
+            ids, sc, cnt = out
+        st = N.qvg_stats()
+        _check(N.lib().qvg_search(self._h, N.ptr(q), nq, k, ef, N.ptr(ids), N.ptr(sc),
+                                  N.ptr(cnt), None, C.byref(st) if stats else None))
+        if stats:
+            return ids, sc, cnt, st.to_dict()
+        return ids, sc, cnt
+
+    def search_ex(self, queries, k=10, ef=64, visited_slots=0, tie_capacity=0,
+                  exact_visited=False, entry_point=None, rerank=True, pools=True,
+                  counters=True, check=True):
+        """Everything: results, per-query status, pool (ids+dists), counters, stats."""
+        q = _f32(queries, self.dim)
+        nq = q.shape[0]
+        opts = N.qvg_search_opts(visited_slots=visited_slots, tie_capacity=tie_capacity,
+                                 exact_visited=int(exact_visited),
+                                 entry_point=SENTINEL if entry_point is None else entry_point,
+                                 no_rerank=int(not rerank))
+        ids = np.empty((nq, k), np.uint32)
+        sc = np.empty((nq, k), np.float32)
+        cnt = np.empty(nq, np.uint32)
+        qs = np.empty(nq, np.int32)
+        pi = np.empty((nq, ef), np.uint32) if pools else None
+        pd = np.empty((nq, ef), np.uint32) if pools else None
+        pn = np.empty(nq, np.uint32) if pools else None
+        ctr = np.empty((nq, 8), np.uint32) if counters else None
+        st = N.qvg_stats()
+        rc = N.lib().qvg_search_ex(self._h, q.ctypes.data, nq, k, ef, C.byref(opts),
+                                   ids.ctypes.data if rerank else None,
+                                   sc.ctypes.data if rerank else None,
+                                   cnt.ctypes.data if rerank else None, qs.ctypes.data,
+                                   N.ptr(pi), N.ptr(pd), N.ptr(pn), N.ptr(ctr), C.byref(st))
+        if check:
+            _check(rc)
+        out = dict(rc=rc, status=qs, stats=st.to_dict())
+        if rerank:
+            out.update(ids=ids, scores=sc, count=cnt)
+        if pools:
+            out.update(pool_ids=pi, pool_dists=pd, pool_n=pn)
+        if counters:
+            out.update(counters=ctr)
+        return out
+
+    def beam_search(self, query_codes, ef, entry_point=None):
+        """beam_search_words on given code words (nq x 2W u64, reference layout)
+        -> (pool_ids[nq,ef], pool_dists[nq,ef], pool_n[nq])."""
+        qc = np.ascontiguousarray(query_codes, np.uint64).reshape(-1, 2 * self.W)
+        nq = qc.shape[0]
+        pi = np.empty((nq, ef), np.uint32)
+        pd = np.empty((nq, ef), np.uint32)
+        pn = np.empty(nq, np.uint32)
+        _check(N.lib().qvg_beam_search(self._h, qc.ctypes.data, nq, ef,
+                                       SENTINEL if entry_point is None else entry_point,
+                                       pi.ctypes.data, pd.ctypes.data, pn.ctypes.data, None))
+        return pi, pd, pn
+
+    def sm2_distance(self, query_codes, ids):
+        qc = np.ascontiguousarray(query_codes, np.uint64).reshape(-1, 2 * self.W)
+        ids = np.ascontiguousarray(ids, np.uint32).reshape(-1)
+        out = np.empty(ids.size, np.uint32)
+        _check(N.lib().qvg_sm2_distance(self._h, qc.ctypes.data, ids.ctypes.data, ids.size,
+                                        out.ctypes.data))
+        return out
+
+
+def encode_queries(x, device=0):
+    """Query-path encode on the GPU -> (normalized[nq,dim], codes[nq,2W], tau[nq]).
+    Raises InvalidArgument like normalize_l2 / encode_sm2_into would."""
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim == 1:
+        x = x.reshape(1, -1)
+    nq, dim = x.shape
+    qn = np.empty((nq, dim), np.float32)
+    codes = np.empty((nq, 2 * words_for_dim(dim)), np.uint64)
+    tau = np.empty(nq, np.float32)
+    st = np.empty(nq, np.int32)
+    _check(N.lib().qvg_encode(device, x.ctypes.data, nq, dim, qn.ctypes.data, codes.ctypes.data,
+                              tau.ctypes.data, st.ctypes.data))
+    return qn, codes, tau
+
+
+def run_query_batch(index: GpuIndex, queries, params: SearchParams, threads=None
+                    ) -> List[SearchResult]:
+    """eval.cpp:225-247: results[i] = query(index, queries[i]) for every query,
+    output order = input order.  `threads` is accepted for signature parity and
+    ignored (one GPU launch serves the batch)."""
+    params.validate()
+    ids, sc, cnt = index.search(queries, params.k, params.ef)
+    return [SearchResult(ids[i, : cnt[i]].copy(), sc[i, : cnt[i]].copy())
+            for i in range(ids.shape[0])]
+
+
+def query(index: GpuIndex, vec, params: SearchParams) -> SearchResult:
+    """search.cpp:122-143 (single query, same error behaviour)."""
+    params.validate()
+    v = np.asarray(vec, dtype=np.float32).reshape(-1)
+    if v.size != index.dim:
+        raise InvalidArgument("query: dimension mismatch")
+    return run_query_batch(index, v.reshape(1, -1), params)[0]

@@ -1,0 +1,458 @@
+// C-ABI entry points for the query path (qvg.h).  Host side of the boundary:
+// argument validation with the reference's error classes, host/device buffer
+// handling, kernel sequencing on the handle's stream, counters.
+//
+// qvg_search mirrors qivr::run_query_batch (eval.cpp:225-247) over
+// qivr::query (search.cpp:122-143): validate params (search.hpp:16-19), per
+// query finite check, normalise, encode, beam search from the entry point,
+// rerank to k.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qvg_internal.cuh"
+
+namespace qvg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+qvg_status cuda_status(cudaError_t e, const char* what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    cudaGetLastError();  // clear sticky-free errors
+    return e == cudaErrorMemoryAllocation ? QVG_OUT_OF_MEMORY : QVG_CUDA_ERROR;
+}
+
+qvg_status grow(Buffer& b, size_t bytes) {
+    if (bytes <= b.bytes && b.p) return QVG_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(scratch)");
+    b.bytes = want;
+    return QVG_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+namespace {
+
+const char* qstatus_message(int32_t s) {
+    switch (s) {
+        case QVG_Q_NONFINITE_COORD: return "query: non-finite coordinate";
+        case QVG_Q_BAD_NORM: return "normalize_l2: zero or non-finite norm";
+        case QVG_Q_NONFINITE_CODE: return "encode: non-finite coordinate";
+        case QVG_Q_TIE_OVERFLOW: return "search: tie stack overflow (raise tie_capacity)";
+        default: return "ok";
+    }
+}
+
+uint32_t log2_floor(uint32_t x) {
+    uint32_t l = 0;
+    while ((1u << (l + 1)) <= x) ++l;
+    return l;
+}
+
+// Output buffer: the user's device pointer, or a scratch buffer copied back to
+// the user's host pointer at the end.
+struct Out {
+    void* user = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+    bool copy_back = false;
+};
+
+qvg_status bind_out(Out& o, void* user, Buffer& scratch, size_t bytes, bool needed) {
+    o.user = user;
+    o.bytes = bytes;
+    if (!user && !needed) return QVG_OK;
+    if (user && is_device_ptr(user)) {
+        o.dev = user;
+        return QVG_OK;
+    }
+    qvg_status st = grow(scratch, bytes);
+    if (st != QVG_OK) return st;
+    o.dev = scratch.p;
+    o.copy_back = user != nullptr;
+    return QVG_OK;
+}
+
+struct Mode {
+    bool encode;   // queries are float vectors (else reference-layout code words)
+    bool rerank;
+};
+
+qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint64_t nq,
+               uint32_t k, uint32_t ef, const qvg_search_opts* opts, Mode mode,
+               uint32_t* out_ids, float* out_scores, uint32_t* out_count,
+               int32_t* out_query_status, uint32_t* out_pool_ids, uint32_t* out_pool_dists,
+               uint32_t* out_pool_size, uint32_t* out_qctr, qvg_stats* stats) {
+    if (!h) {
+        set_error("qvg_search: null index");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (mode.rerank) {
+        if (k < 1) {
+            set_error("SearchParams: k must be >= 1");
+            return QVG_INVALID_ARGUMENT;
+        }
+        if (ef < k) {
+            set_error("SearchParams: ef must be >= k");
+            return QVG_INVALID_ARGUMENT;
+        }
+    } else if (ef < 1) {
+        set_error("beam_search: ef must be >= 1");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (ef > kMaxEf) {
+        set_error("search: ef > " + std::to_string(kMaxEf) + " is not supported");
+        return QVG_NOT_IMPLEMENTED;
+    }
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (nq == 0) return QVG_OK;
+    if (!queries && !qcodes) {
+        set_error("qvg_search: null queries");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (mode.rerank && (!out_ids || !out_scores || !out_count)) {
+        set_error("qvg_search: out_ids, out_scores and out_count are required");
+        return QVG_INVALID_ARGUMENT;
+    }
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    const DevIndex& ix = h->ix;
+    cudaStream_t s = h->stream;
+    const uint32_t entry =
+        opts && opts->entry_point != kSentinel ? opts->entry_point : ix.entry;
+    if (entry >= ix.n) {
+        set_error("beam_search: invalid entry point");
+        return QVG_INVALID_ARGUMENT;
+    }
+    uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
+    if (!vslots) vslots = ef <= 64 ? 1024u : (ef <= 128 ? 2048u : 4096u);
+    if (vslots < 32 * ((ef + 31) / 32)) vslots = 32 * ((ef + 31) / 32);  // scores alias it
+    uint32_t vlog = log2_floor(vslots);
+    if ((1u << vlog) < vslots) ++vlog;
+    if (vlog < 5) vlog = 5;
+    uint32_t tcap = opts && opts->tie_capacity ? opts->tie_capacity : (ef < 64 ? 64u : ef);
+    tcap = (tcap + 3) & ~3u;
+    const bool exact = opts && opts->exact_visited;
+    const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
+    const bool want_ctr = stats != nullptr || out_qctr != nullptr;
+
+    qvg_status st = QVG_OK;
+    // ---- inputs -------------------------------------------------------------
+    const size_t in_bytes = mode.encode ? nq * (size_t)ix.dim * 4 : nq * 2ull * ix.W * 8;
+    const void* user_in = mode.encode ? (const void*)queries : (const void*)qcodes;
+    const bool in_dev = is_device_ptr(user_in);
+    if ((st = grow(h->s_qn, nq * (size_t)ix.Dp * 4)) != QVG_OK) return st;
+    if ((st = grow(h->s_qc, nq * (size_t)ix.W * 16)) != QVG_OK) return st;
+    if ((st = grow(h->s_qst, nq * 4 + 16)) != QVG_OK) return st;  // + flag word
+    if ((st = grow(h->s_counter, 64)) != QVG_OK) return st;
+    if (!in_dev && (st = grow(h->s_in, in_bytes)) != QVG_OK) return st;
+    Out o_ids, o_sc, o_cnt, o_st, o_pi, o_pd, o_pn, o_ctr;
+    if ((st = bind_out(o_ids, out_ids, h->s_ids, nq * k * 4ull, do_rerank)) != QVG_OK) return st;
+    if ((st = bind_out(o_sc, out_scores, h->s_sc, nq * k * 4ull, do_rerank)) != QVG_OK) return st;
+    if ((st = bind_out(o_cnt, out_count, h->s_cnt, nq * 4ull, do_rerank)) != QVG_OK) return st;
+    if ((st = bind_out(o_st, out_query_status, h->s_st, nq * 4ull, true)) != QVG_OK) return st;
+    if ((st = bind_out(o_pi, out_pool_ids, h->s_pool_i, nq * ef * 4ull, false)) != QVG_OK) return st;
+    if ((st = bind_out(o_pd, out_pool_dists, h->s_pool_d, nq * ef * 4ull, o_pi.dev != nullptr)) != QVG_OK) return st;
+    if ((st = bind_out(o_pn, out_pool_size, h->s_pool_n, nq * 4ull, o_pi.dev != nullptr)) != QVG_OK) return st;
+    if ((st = bind_out(o_ctr, out_qctr, h->s_qctr, nq * 32ull, want_ctr)) != QVG_OK) return st;
+
+    SearchLaunch a{};
+    a.ix = ix;
+    a.qcodes = static_cast<const uint4*>(h->s_qc.p);
+    a.qn = static_cast<const float*>(h->s_qn.p);
+    a.qstatus = static_cast<const int32_t*>(h->s_qst.p);
+    a.nq = nq;
+    a.ef = ef;
+    a.k = k;
+    a.entry = entry;
+    a.vis_log2 = vlog;
+    a.tie_cap = tcap;
+    a.do_rerank = do_rerank;
+    a.out_ids = static_cast<uint32_t*>(o_ids.dev);
+    a.out_scores = static_cast<float*>(o_sc.dev);
+    a.out_count = static_cast<uint32_t*>(o_cnt.dev);
+    a.out_status = static_cast<int32_t*>(o_st.dev);
+    a.pool_ids = static_cast<uint32_t*>(o_pi.dev);
+    a.pool_dists = static_cast<uint32_t*>(o_pd.dev);
+    a.pool_n = static_cast<uint32_t*>(o_pn.dev);
+    a.qctr = static_cast<uint32_t*>(o_ctr.dev);
+    a.counter = static_cast<unsigned long long*>(h->s_counter.p);
+    uint64_t grid = 0;
+    if ((st = plan_search(a, h->device, &grid)) != QVG_OK) return st;
+    if (exact) {
+        const uint64_t words = ((ix.n + 31) / 32 + 3) & ~3ull;
+        if ((st = grow(h->s_exact, grid * kWarpsPerBlock * words * 4)) != QVG_OK) return st;
+        a.exact_bits = static_cast<uint32_t*>(h->s_exact.p);
+        a.exact_words = words;
+    }
+
+    // ---- pipeline -------------------------------------------------------------
+    cudaEventRecord(h->ev[0], s);
+    const void* din = user_in;
+    if (!in_dev) {
+        e = cudaMemcpyAsync(h->s_in.p, user_in, in_bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_status(e, "H2D(queries)");
+        din = h->s_in.p;
+    }
+    cudaMemsetAsync(h->s_counter.p, 0, 64, s);
+    cudaEventRecord(h->ev[1], s);
+    if (mode.encode) {
+        launch_encode(static_cast<const float*>(din), nq, ix.dim, ix.Dp,
+                      static_cast<float*>(h->s_qn.p), static_cast<uint4*>(h->s_qc.p), nullptr,
+                      static_cast<int32_t*>(h->s_qst.p), s);
+    } else {
+        launch_codes_to_chunks(static_cast<const uint64_t*>(din), nq, ix.W,
+                               static_cast<uint4*>(h->s_qc.p), s);
+        cudaMemsetAsync(h->s_qst.p, 0, nq * 4, s);
+    }
+    cudaEventRecord(h->ev[2], s);
+    if ((st = launch_search(a, grid, s)) != QVG_OK) return st;
+    cudaEventRecord(h->ev[3], s);
+    Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
+    for (Out* o : outs) {
+        if (o->copy_back) {
+            e = cudaMemcpyAsync(o->user, o->dev, o->bytes, cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_status(e, "D2H(results)");
+        }
+    }
+    // status summary (copied even when the caller did not ask for statuses)
+    std::vector<int32_t> qst_host;
+    int32_t* qst_view = nullptr;
+    if (o_st.copy_back) {
+        qst_view = out_query_status;
+    } else {
+        qst_host.resize(nq);
+        e = cudaMemcpyAsync(qst_host.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
+        qst_view = qst_host.data();
+    }
+    std::vector<uint32_t> ctr_host;
+    if (stats && !o_ctr.copy_back) {
+        ctr_host.resize(nq * 8);
+        e = cudaMemcpyAsync(ctr_host.data(), o_ctr.dev, nq * 32, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_status(e, "D2H(counters)");
+    }
+    cudaEventRecord(h->ev[4], s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "search");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_status(e, "search");
+
+    if (stats) {
+        float t = 0;
+        cudaEventElapsedTime(&t, h->ev[1], h->ev[2]);
+        stats->encode_ms = t;
+        cudaEventElapsedTime(&t, h->ev[2], h->ev[3]);
+        stats->search_ms = t;
+        cudaEventElapsedTime(&t, h->ev[1], h->ev[3]);
+        stats->device_ms = t;
+        cudaEventElapsedTime(&t, h->ev[0], h->ev[4]);
+        stats->total_ms = t;
+        const uint32_t* c = o_ctr.copy_back ? out_qctr : ctr_host.data();
+        stats->queries = nq;
+        for (uint64_t i = 0; i < nq; ++i) {
+            const uint32_t* r = c + i * 8;
+            if (r[7] == QVG_Q_NONFINITE_COORD || r[7] == QVG_Q_BAD_NORM ||
+                r[7] == QVG_Q_NONFINITE_CODE)
+                continue;
+            stats->expansions += r[0];
+            stats->tie_expansions += r[1];
+            stats->dist_evals += r[2];
+            stats->inpool_drops += r[3];
+            stats->adjacency_slots += r[4];
+            stats->cold_accesses += do_rerank ? r[5] : 0;
+            stats->tie_overflows += r[7] == QVG_Q_TIE_OVERFLOW;
+            if (r[6] > stats->max_tie_depth) stats->max_tie_depth = r[6];
+            stats->adjacency_bytes += 4ull * r[0] + 4ull * r[4];
+        }
+        stats->code_bytes = stats->dist_evals * 16ull * ix.W;
+        stats->rerank_bytes = stats->cold_accesses * 4ull * ix.dim;
+        stats->io_bytes = nq * (4ull * ix.dim + (do_rerank ? 8ull * k : 0));
+    }
+    // overall status: first invalid query (the reference's single-threaded
+    // batch throws at the first one), else tie overflow
+    int64_t first_bad = -1, first_ovf = -1;
+    for (uint64_t i = 0; i < nq; ++i) {
+        const int32_t v = qst_view[i];
+        if (v == QVG_Q_TIE_OVERFLOW) {
+            if (first_ovf < 0) first_ovf = (int64_t)i;
+        } else if (v != 0 && first_bad < 0) {
+            first_bad = (int64_t)i;
+        }
+    }
+    if (first_bad >= 0) {
+        set_error(std::string(qstatus_message(qst_view[first_bad])) + " (query " +
+                  std::to_string(first_bad) + ")");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (first_ovf >= 0) {
+        set_error(std::string(qstatus_message(QVG_Q_TIE_OVERFLOW)) + " (query " +
+                  std::to_string(first_ovf) + ")");
+        return QVG_CAPACITY_OVERFLOW;
+    }
+    return QVG_OK;
+}
+
+}  // namespace
+}  // namespace qvg
+
+using namespace qvg;
+
+extern "C" {
+
+const char* qvg_last_error(void) { return g_last_error.c_str(); }
+
+int qvg_abi_version(void) { return QVG_ABI_VERSION; }
+
+qvg_status qvg_search(qvg_index* index, const float* queries, uint64_t nq, uint32_t k,
+                      uint32_t ef, uint32_t* out_ids, float* out_scores, uint32_t* out_count,
+                      int32_t* out_query_status, qvg_stats* stats) {
+    return run(index, queries, nullptr, nq, k, ef, nullptr, Mode{true, true}, out_ids,
+               out_scores, out_count, out_query_status, nullptr, nullptr, nullptr, nullptr,
+               stats);
+}
+
+qvg_status qvg_search_ex(qvg_index* index, const float* queries, uint64_t nq, uint32_t k,
+                         uint32_t ef, const qvg_search_opts* opts, uint32_t* out_ids,
+                         float* out_scores, uint32_t* out_count, int32_t* out_query_status,
+                         uint32_t* out_pool_ids, uint32_t* out_pool_dists,
+                         uint32_t* out_pool_size, uint32_t* out_query_counters,
+                         qvg_stats* stats) {
+    const bool rr = !(opts && opts->no_rerank);
+    return run(index, queries, nullptr, nq, k, ef, opts, Mode{true, rr}, out_ids, out_scores,
+               out_count, out_query_status, out_pool_ids, out_pool_dists, out_pool_size,
+               out_query_counters, stats);
+}
+
+qvg_status qvg_beam_search(qvg_index* index, const uint64_t* query_codes, uint64_t nq,
+                           uint32_t ef, uint32_t entry_point, uint32_t* out_pool_ids,
+                           uint32_t* out_pool_dists, uint32_t* out_pool_size,
+                           qvg_stats* stats) {
+    qvg_search_opts o{};
+    o.entry_point = entry_point;
+    o.no_rerank = 1;
+    if (!out_pool_ids || !out_pool_dists || !out_pool_size) {
+        set_error("qvg_beam_search: pool outputs are required");
+        return QVG_INVALID_ARGUMENT;
+    }
+    return run(index, nullptr, query_codes, nq, 1, ef, &o, Mode{false, false}, nullptr,
+               nullptr, nullptr, nullptr, out_pool_ids, out_pool_dists, out_pool_size, nullptr,
+               stats);
+}
+
+qvg_status qvg_encode(int device, const float* x, uint64_t nq, uint32_t dim,
+                      float* out_normalized, uint64_t* out_codes, float* out_tau,
+                      int32_t* out_query_status) {
+    if (dim == 0) {
+        set_error("compute_threshold: empty vector");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (nq == 0) return QVG_OK;
+    if (!x || !out_normalized || !out_codes || !out_query_status) {
+        set_error("qvg_encode: null argument");
+        return QVG_INVALID_ARGUMENT;
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    const uint32_t W = (dim + 63) / 64, Dp = (dim + 3) & ~3u;
+    void *d_x = nullptr, *d_qn = nullptr, *d_qc = nullptr, *d_codes = nullptr, *d_tau = nullptr,
+         *d_st = nullptr;
+    e = cudaMalloc(&d_x, nq * dim * 4ull);
+    if (e == cudaSuccess) e = cudaMalloc(&d_qn, nq * Dp * 4ull);
+    if (e == cudaSuccess) e = cudaMalloc(&d_qc, nq * W * 16ull);
+    if (e == cudaSuccess) e = cudaMalloc(&d_codes, nq * W * 16ull);
+    if (e == cudaSuccess) e = cudaMalloc(&d_tau, nq * 4ull);
+    if (e == cudaSuccess) e = cudaMalloc(&d_st, nq * 4ull);
+    if (e == cudaSuccess) e = cudaMemcpy(d_x, x, nq * dim * 4ull, cudaMemcpyDefault);
+    if (e == cudaSuccess) {
+        launch_encode(static_cast<const float*>(d_x), nq, dim, Dp, static_cast<float*>(d_qn),
+                      static_cast<uint4*>(d_qc), static_cast<float*>(d_tau),
+                      static_cast<int32_t*>(d_st), 0);
+        launch_chunks_to_codes(static_cast<const uint4*>(d_qc), nq, W,
+                               static_cast<uint64_t*>(d_codes), 0);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpy2D(out_normalized, dim * 4ull, d_qn, Dp * 4ull, dim * 4ull, nq,
+                         cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(out_codes, d_codes, nq * W * 16ull, cudaMemcpyDefault);
+    if (e == cudaSuccess && out_tau) e = cudaMemcpy(out_tau, d_tau, nq * 4ull, cudaMemcpyDefault);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(out_query_status, d_st, nq * 4ull, cudaMemcpyDefault);
+    cudaFree(d_x);
+    cudaFree(d_qn);
+    cudaFree(d_qc);
+    cudaFree(d_codes);
+    cudaFree(d_tau);
+    cudaFree(d_st);
+    if (e != cudaSuccess) return cuda_status(e, "qvg_encode");
+    std::vector<int32_t> sts(nq);
+    if (is_device_ptr(out_query_status))
+        cudaMemcpy(sts.data(), out_query_status, nq * 4, cudaMemcpyDeviceToHost);
+    else
+        std::memcpy(sts.data(), out_query_status, nq * 4);
+    for (uint64_t i = 0; i < nq; ++i)
+        if (sts[i] != 0) {
+            set_error(std::string(qstatus_message(sts[i])) + " (row " + std::to_string(i) + ")");
+            return QVG_INVALID_ARGUMENT;
+        }
+    return QVG_OK;
+}
+
+qvg_status qvg_sm2_distance(qvg_index* h, const uint64_t* query_codes, const uint32_t* ids,
+                            uint64_t npairs, uint32_t* out) {
+    if (!h || !query_codes || !ids || !out) {
+        set_error("qvg_sm2_distance: null argument");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (npairs == 0) return QVG_OK;
+    cudaSetDevice(h->device);
+    const DevIndex& ix = h->ix;
+    std::vector<uint32_t> hid(npairs);
+    cudaError_t e = cudaMemcpy(hid.data(), ids, npairs * 4, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_status(e, "qvg_sm2_distance");
+    for (uint64_t i = 0; i < npairs; ++i)
+        if (hid[i] >= ix.n) {
+            set_error("sm2_distance: node id out of range");
+            return QVG_INVALID_ARGUMENT;
+        }
+    qvg_status st;
+    if ((st = grow(h->s_in, npairs * 2ull * ix.W * 8)) != QVG_OK) return st;
+    if ((st = grow(h->s_qc, npairs * (size_t)ix.W * 16)) != QVG_OK) return st;
+    if ((st = grow(h->s_pair_ids, npairs * 4)) != QVG_OK) return st;
+    if ((st = grow(h->s_pair_out, npairs * 4)) != QVG_OK) return st;
+    cudaStream_t s = h->stream;
+    e = cudaMemcpyAsync(h->s_in.p, query_codes, npairs * 2ull * ix.W * 8, cudaMemcpyDefault, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->s_pair_ids.p, hid.data(), npairs * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "qvg_sm2_distance");
+    launch_codes_to_chunks(static_cast<const uint64_t*>(h->s_in.p), npairs, ix.W,
+                           static_cast<uint4*>(h->s_qc.p), s);
+    launch_pair_distance(ix, static_cast<const uint4*>(h->s_qc.p),
+                         static_cast<const uint32_t*>(h->s_pair_ids.p), npairs,
+                         static_cast<uint32_t*>(h->s_pair_out.p), s);
+    e = cudaMemcpyAsync(out, h->s_pair_out.p, npairs * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? QVG_OK : cuda_status(e, "qvg_sm2_distance");
+}
+
+}  // extern "C"

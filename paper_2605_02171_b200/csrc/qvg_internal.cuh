@@ -1,0 +1,98 @@
+// Internal declarations shared by the qvg translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/qvg.h"
+
+namespace qvg {
+
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr uint32_t kMaxEf = 1024;
+constexpr uint32_t kMaxDegree = 128;
+constexpr int kWarpsPerBlock = 4;
+
+// HBM-resident index.  Layouts:
+//   codes : n x W chunks of 16 B, chunk w = {pos word w, strong word w}
+//   adj   : n x RS u32 (RS = R rounded up to 4), deduplicated, row order kept,
+//           unused slots = kSentinel (degree is implicit)
+//   cold  : n x Dp f32 (Dp = dim rounded up to 4, zero pad)
+struct DevIndex {
+    const uint4* codes;
+    const uint32_t* adj;
+    const float* cold;
+    uint64_t n;
+    uint32_t dim, W, R, RS, Dp, entry;
+};
+
+struct Buffer {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace qvg
+
+struct qvg_index {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    qvg::DevIndex ix{};
+    uint32_t m = 0;       // params.m (R = 2m for reference-built graphs)
+    float alpha = 1.2f;
+    void* d_codes = nullptr;
+    void* d_adj = nullptr;
+    void* d_cold = nullptr;
+    // scratch, grown on demand
+    qvg::Buffer s_in, s_qn, s_qc, s_qst, s_ids, s_sc, s_cnt, s_pool_i, s_pool_d, s_pool_n,
+        s_qctr, s_counter, s_exact, s_pair_ids, s_pair_out, s_st;
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace qvg {
+
+void set_error(const std::string& msg);
+qvg_status cuda_status(cudaError_t e, const char* what);
+qvg_status grow(Buffer& b, size_t bytes);
+bool is_device_ptr(const void* p);
+
+// kernels (encode.cu / search.cu)
+void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float* qn,
+                   uint4* qcodes, float* tau, int32_t* status, cudaStream_t s);
+void launch_codes_to_chunks(const uint64_t* ref_codes, uint64_t rows, uint32_t W, uint4* out,
+                            cudaStream_t s);
+void launch_chunks_to_codes(const uint4* chunks, uint64_t rows, uint32_t W, uint64_t* out,
+                            cudaStream_t s);
+
+struct SearchLaunch {
+    DevIndex ix;
+    const uint4* qcodes;
+    const float* qn;
+    const int32_t* qstatus;
+    uint64_t nq;
+    uint32_t ef, k, entry;
+    uint32_t vis_log2, tie_cap;
+    uint32_t do_rerank;
+    uint32_t* out_ids;
+    float* out_scores;
+    uint32_t* out_count;
+    int32_t* out_status;
+    uint32_t* pool_ids;
+    uint32_t* pool_dists;
+    uint32_t* pool_n;
+    uint32_t* qctr;
+    unsigned long long* counter;
+    uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
+    uint64_t exact_words;   // words per slot
+};
+
+// grid = min(resident blocks, ceil(nq / warps per block)); exact-visited
+// bitmaps are sized for grid * kWarpsPerBlock warp slots.
+qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid);
+qvg_status launch_search(const SearchLaunch& a, uint64_t grid, cudaStream_t s);
+void launch_pair_distance(const DevIndex& ix, const uint4* qchunks, const uint32_t* ids,
+                          uint64_t npairs, uint32_t* out, cudaStream_t s);
+
+}  // namespace qvg

@@ -1,0 +1,290 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference's
+golden fixtures, the compiled reference (oracle/_ref) and the C restatement.
+Bar: bit-exact codes, distances, pools (ids + dists), result ids and score bit
+patterns."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")
+
+import paper_2605_02171_b200 as Q  # noqa: E402
+
+
+def gpu_index_from_golden(g):
+    return Q.GpuIndex.from_arrays(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+
+
+# ---------------------------------------------------------------- K1 encode
+def test_encode_known_answers(known_answers):
+    for e in known_answers["query_encodings"]:
+        x = np.array(e["x"], np.uint32).view(np.float32)
+        qn, codes, tau = Q.encode_queries(x)
+        assert qn[0].view(np.uint32).tolist() == e["norm"], e["dim"]
+        assert [int(v) for v in codes[0]] == e["code"], e["dim"]
+        assert np.float32(tau[0]) == np.float32(e["tau"])
+
+
+@pytest.mark.parametrize("dim", [1, 4, 63, 64, 65, 99, 100, 384, 768, 1023, 1536, 3072])
+def test_encode_bit_exact_vs_oracle(dim):
+    rng = np.random.Generator(np.random.PCG64(dim))
+    x = rng.standard_normal((257, dim)).astype(np.float32)
+    x[7] *= 1e-30  # tiny magnitudes (denormal-range products)
+    x[8] *= 1e30
+    qn, codes, tau = Q.encode_queries(x)
+    for i in range(x.shape[0]):
+        n2, c2, t2 = O.orc_encode_query(x[i])
+        assert np.array_equal(qn[i].view(np.uint32), n2.view(np.uint32)), i
+        assert np.array_equal(codes[i], c2), i
+        assert np.float32(tau[i]).view(np.uint32) == np.float32(t2).view(np.uint32)
+
+
+def test_encode_errors_like_reference():
+    x = np.ones((4, 16), np.float32)
+    x[1] = 0.0
+    with pytest.raises(Q.InvalidArgument, match="zero or non-finite norm"):
+        Q.encode_queries(x)
+    x[1] = 1.0
+    x[2, 3] = np.nan
+    with pytest.raises(Q.InvalidArgument, match="non-finite coordinate"):
+        Q.encode_queries(x)
+
+
+# ---------------------------------------------------------------- K2 distance
+@pytest.mark.parametrize("dim", [4, 63, 64, 65, 100, 384, 768, 1023])
+def test_sm2_distance_bit_exact(dim):
+    rng = np.random.Generator(np.random.PCG64(100 + dim))
+    n = 300
+    base = rng.standard_normal((n, dim)).astype(np.float32)
+    codes = np.stack([O.ref_encode_raw(b)[0] if O.ref_available() else
+                      O.orc_encode_query(b)[1] for b in base])
+    cold = base / np.linalg.norm(base, axis=1, keepdims=True)
+    adj = np.zeros((n, 3), np.uint32)
+    ix = Q.GpuIndex.from_arrays(codes, adj, cold, 0)
+    qc = np.stack([O.orc_encode_query(v)[1] for v in rng.standard_normal((160, dim)).astype(np.float32)])
+    ids = rng.integers(0, n, 160).astype(np.uint32)
+    got = ix.sm2_distance(qc, ids)
+    want = np.array([O.orc_sm2(qc[i], codes[ids[i]]) for i in range(160)])
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------- K3 + K4
+@pytest.mark.parametrize("name", ["g1", "g2", "g3"])
+def test_golden_pools_ids_scores(name):
+    g = load_golden(name)
+    ix = gpu_index_from_golden(g)
+    k = int(g["k"])
+    for ef in g["efs"]:
+        ef = int(ef)
+        for vslots in (0, 32):
+            r = ix.search_ex(g["queries"], k=k, ef=ef, visited_slots=vslots)
+            assert np.array_equal(r["pool_n"], g[f"pool_n_{ef}"]), (name, ef)
+            assert np.array_equal(r["pool_ids"], g[f"pool_ids_{ef}"]), (name, ef)
+            assert np.array_equal(r["pool_dists"], g[f"pool_dists_{ef}"]), (name, ef)
+            assert np.array_equal(r["count"], g[f"count_{ef}"]), (name, ef)
+            assert np.array_equal(r["ids"], g[f"ids_{ef}"]), (name, ef)
+            assert np.array_equal(r["scores"].view(np.uint32), g[f"scores_{ef}"]), (name, ef)
+            assert (r["status"] == 0).all()
+            # cold-access bound (acceptance_main.cpp:416-432): == pool size <= ef
+            assert r["stats"]["cold_accesses"] == int(g[f"pool_n_{ef}"].sum())
+            assert (r["pool_n"] <= ef).all()
+
+
+@pytest.mark.parametrize("name", ["g1", "g2", "g3"])
+def test_exact_visited_mode_matches_oracle_counters(name):
+    g = load_golden(name)
+    ix = gpu_index_from_golden(g)
+    orc = O.OracleIndex(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    k = int(g["k"])
+    for ef in g["efs"]:
+        ef = int(ef)
+        r = ix.search_ex(g["queries"], k=k, ef=ef, exact_visited=True)
+        o = orc.query_batch(g["queries"], ef, k, mode=0)
+        assert np.array_equal(r["ids"], o["ids"])
+        s = r["stats"]
+        assert s["expansions"] == o["stats"]["expansions"]
+        assert s["tie_expansions"] == o["stats"]["tie_expansions"]
+        assert s["dist_evals"] == o["stats"]["dist_evals"]
+        assert s["inpool_drops"] == 0
+
+
+def test_beam_search_with_given_codes_and_entry():
+    g = load_golden("g1")
+    ix = gpu_index_from_golden(g)
+    qc = np.stack([O.orc_encode_query(q)[1] for q in g["queries"]])
+    pi, pd, pn = ix.beam_search(qc, 32)
+    assert np.array_equal(pn, g["pool_n_32"])
+    assert np.array_equal(pi, g["pool_ids_32"])
+    assert np.array_equal(pd, g["pool_dists_32"])
+
+
+def test_ef_ge_n_equals_bruteforce_bq_ranking():
+    """test_search.cpp:70-118 restated: with ef >= N the pool is the brute-force
+    BQ ranking of every node reachable from the entry point."""
+    g = load_golden("g2")
+    n = g["cold"].shape[0]
+    ix = gpu_index_from_golden(g)
+    adj = g["adj"]
+    reach = np.zeros(n, bool)
+    stack = [int(g["entry"])]
+    reach[stack[0]] = True
+    while stack:
+        u = stack.pop()
+        for v in adj[u, 1:1 + adj[u, 0]]:
+            if not reach[v]:
+                reach[v] = True
+                stack.append(int(v))
+    qc = np.stack([O.orc_encode_query(q)[1] for q in g["queries"][:20]])
+    pi, pd, pn = ix.beam_search(qc, 1024)
+    for i in range(20):
+        keys = sorted((O.orc_sm2(qc[i], g["codes"][j]), j) for j in np.nonzero(reach)[0])
+        assert pn[i] == len(keys)
+        assert pi[i, : pn[i]].tolist() == [j for _, j in keys]
+        assert pd[i, : pn[i]].tolist() == [d for d, _ in keys]
+
+
+def _tiny_index(vectors, edges, m, entry):
+    """make_index of test_search.cpp:18-40 (own code): normalise, encode, slots."""
+    vecs = np.array(vectors, np.float32)
+    cold = np.stack([O.orc_encode_query(v)[0] for v in vecs])
+    codes = np.stack([O.orc_encode_query(v)[1] for v in vecs])
+    # node codes are encode_sm2 of the *normalised* vector (stage0): re-encode raw
+    adj = np.zeros((len(vecs), 2 * m + 1), np.uint32)
+    for u, e in enumerate(edges):
+        adj[u, 0] = len(e)
+        adj[u, 1:1 + len(e)] = e
+    return Q.GpuIndex.from_arrays(codes, adj, cold, entry), cold, codes
+
+
+def test_path_graph_known_answer():
+    # test_search.cpp:44-59: 0-1-2 chain, query = node 2's vector, ef=3
+    ix, cold, codes = _tiny_index([[1.0, 0.0, 0.2], [0.6, 0.6, 0.2], [0.0, 1.0, 0.2]],
+                                  [[1], [0, 2], [1]], 2, 0)
+    pi, pd, pn = ix.beam_search(codes[2:3], 3)
+    assert pn[0] == 3 and pi[0, 0] == 2 and pd[0, 0] == 0
+
+
+def test_single_node_graph():
+    ix, cold, codes = _tiny_index([[0.3, 0.4]], [[]], 2, 0)
+    res = Q.query(ix, [0.6, 0.8], Q.SearchParams(ef=4, k=1))
+    assert res.ids.tolist() == [0]
+
+
+def test_rerank_tie_break_known_answer():
+    # test_search.cpp:140-162: ids 0 and 3 identical -> lower id first
+    vecs = [[1.0, 0.0], [0.9, 0.1], [0.0, 1.0], [1.0, 0.0]]
+    edges = [[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]]
+    ix, cold, codes = _tiny_index(vecs, edges, 2, 0)
+    r = Q.query(ix, [1.0, 0.0], Q.SearchParams(ef=4, k=4))
+    assert r.ids.tolist() == [0, 3, 1, 2]
+    assert abs(r.scores[0] - 1.0) < 1e-6
+    assert np.all(np.diff(r.scores) <= 0)
+    r2 = Q.query(ix, [1.0, 0.0], Q.SearchParams(ef=10, k=10))
+    assert len(r2.ids) == 4  # k > |pool| ranks everything
+
+
+def test_query_errors_like_reference():
+    g = load_golden("g1")
+    ix = gpu_index_from_golden(g)
+    sp = Q.SearchParams(64, 1)
+    with pytest.raises(Q.InvalidArgument):
+        Q.query(ix, np.zeros(64, np.float32), sp)
+    bad = np.zeros(64, np.float32)
+    bad[0] = np.nan
+    with pytest.raises(Q.InvalidArgument):
+        Q.query(ix, bad, sp)
+    with pytest.raises(Q.InvalidArgument):
+        Q.query(ix, [1.0], sp)
+    with pytest.raises(Q.InvalidArgument):
+        ix.search(g["queries"], k=0, ef=4)
+    with pytest.raises(Q.InvalidArgument):
+        ix.search(g["queries"], k=5, ef=4)
+    # a batch with one bad row: valid rows answered, bad row flagged
+    q = g["queries"][:8].copy()
+    q[3] = 0
+    r = ix.search_ex(q, k=10, ef=32, check=False)
+    assert r["rc"] == 1 and r["status"][3] == 2 and (np.delete(r["status"], 3) == 0).all()
+    assert np.array_equal(np.delete(r["ids"], 3, 0), np.delete(g["ids_32"][:8], 3, 0))
+
+
+def test_self_query_finds_itself():
+    g = load_golden("g1")
+    ix = gpu_index_from_golden(g)
+    r = Q.query(ix, g["cold"][123], Q.SearchParams(64, 1))
+    assert r.ids.tolist() == [123] and abs(r.scores[0] - 1.0) < 1e-5
+
+
+def test_device_resident_queries_and_outputs():
+    import torch
+    g = load_golden("g1")
+    ix = gpu_index_from_golden(g)
+    q = torch.from_numpy(g["queries"]).cuda()
+    nq = q.shape[0]
+    ids = torch.empty((nq, 10), dtype=torch.int32, device="cuda")
+    sc = torch.empty((nq, 10), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    ix.set_stream(torch.cuda.current_stream())
+    ix.search(q, 10, 32, out=(ids, sc, cnt))
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), g["ids_32"])
+    assert np.array_equal(sc.cpu().numpy().view(np.uint32), g["scores_32"])
+
+
+def test_qivr_file_roundtrip(tmp_path):
+    g = load_golden("g1")
+    ix = gpu_index_from_golden(g)
+    p = tmp_path / "g1.qivr"
+    ix.save(p)
+    ix2 = Q.GpuIndex.load(p)
+    codes, adj, cold = ix2.export()
+    assert np.array_equal(codes, g["codes"]) and np.array_equal(adj, g["adj"])
+    assert np.array_equal(cold, g["cold"])
+    r = ix2.search(g["queries"], 10, 100)
+    assert np.array_equal(r[0], g["ids_100"])
+    # fail closed: bad magic / version / truncation
+    raw = p.read_bytes()
+    for name, blob in (("magic", b"XXXX" + raw[4:]), ("version", raw[:4] + b"\x02" + raw[5:]),
+                       ("trunc", raw[:-4])):
+        bad = tmp_path / f"bad_{name}.qivr"
+        bad.write_bytes(blob)
+        with pytest.raises(Q.QvgRuntimeError):
+            Q.GpuIndex.load(bad)
+
+
+@ref_only
+def test_reference_reads_our_file_and_we_read_theirs(tmp_path):
+    g = load_golden("g2")
+    ref = O.RefIndex.from_parts(g["codes"], g["adj"], g["cold"], 99, int(g["m"]),
+                                int(g["entry"]))
+    p = tmp_path / "ref.qivr"
+    ref.save(p)
+    ix = Q.GpuIndex.load(p)
+    ids, sc, cnt = ix.search(g["queries"], 10, 50)
+    assert np.array_equal(ids, g["ids_50"])
+    p2 = tmp_path / "ours.qivr"
+    ix.save(p2)
+    assert p2.read_bytes() == p.read_bytes()
+
+
+# ---------------------------------------------------------------- fresh graphs
+@ref_only
+@pytest.mark.parametrize("sigma_mode", ["literal", "norm"])
+def test_cfg1_shape_parity_vs_reference(sigma_mode):
+    """Config-1 geometry (D=384, R=32, L=64, alpha=1.2) at N=30K built by the
+    reference (multi-threaded), 1000 queries, ef in {16, 64, 256}: bit-identical
+    ids and scores, identical pools."""
+    from paper_2605_02171_b200.datasets import mixture
+    base, q = mixture(30_000, 384, 300, 0.35, seed=11, nq=1000, sigma_mode=sigma_mode)
+    ref = O.RefIndex.build(base, m=16, ef_c=64, alpha=1.2, threads=os.cpu_count())
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    for ef in (16, 64, 256):
+        ids, sc, cnt = ref.run_query_batch(q, ef, 10, threads=os.cpu_count())
+        r = ix.search_ex(q, k=10, ef=ef)
+        assert np.array_equal(r["ids"], ids), ef
+        assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32)), ef
+        assert r["stats"]["tie_overflows"] == 0

@@ -1,0 +1,151 @@
+"""Pin the CPU oracle (oracle/qvg_oracle.c) before trusting it:
+  * against the reference's own known-answer tests (values restated from
+    tests/test_encoding.cpp:22-107, test_search.cpp:44-68, 140-162),
+  * against the committed golden fixtures produced by the reference library,
+  * against the compiled reference itself (oracle/_ref) on fresh seeded graphs.
+CPU only (no GPU)."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import oracle as O
+
+ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+
+
+def test_encode_worked_example(known_answers):
+    # test_encoding.cpp:22-44: tau 0.425, pos bits 0,2 strong bits 0,2
+    ka = known_answers["encode_worked"]
+    assert abs(ka["tau"] - 0.425) < 1e-6
+    assert ka["code"] == [0b0101, 0b0101]
+    nrm, code, tau = O.orc_encode_query(np.array(ka["x"], np.float32))
+    # normalisation does not change signs or the strong pattern here
+    assert list(code) == ka["code"]
+
+
+def test_encode_strict_inequalities(known_answers):
+    # test_encoding.cpp:46-57
+    assert known_answers["encode_zero"]["code"] == [0, 0]
+    assert known_answers["encode_ones"]["code"] == [0b1111, 0]
+    assert known_answers["encode_ones"]["tau"] == 1.0
+
+
+def test_sm2_known_answers(known_answers):
+    # test_encoding.cpp:81-107: 5, 12, constructed 16
+    dists = [p["dist"] for p in known_answers["sm2_pairs"]]
+    assert dists == [5, 12]
+    c = known_answers["sm2_constructed"]
+    assert c["dist"] == 16
+    assert O.orc_sm2(np.array(c["a"], np.uint64), np.array(c["b"], np.uint64)) == 16
+    for p in known_answers["sm2_pairs"]:
+        _, ca, _ = O.orc_encode_query(np.array(p["a"], np.float32))
+        _, cb, _ = O.orc_encode_query(np.array(p["b"], np.float32))
+        assert O.orc_sm2(ca, cb) == p["dist"]
+
+
+def test_query_encodings_match_reference_golden(known_answers):
+    for e in known_answers["query_encodings"]:
+        x = np.array(e["x"], np.uint32).view(np.float32)
+        nrm, code, tau = O.orc_encode_query(x)
+        assert nrm.view(np.uint32).tolist() == e["norm"], e["dim"]
+        assert [int(v) for v in code] == e["code"], e["dim"]
+        assert np.float32(tau) == np.float32(e["tau"])
+
+
+def test_encode_errors():
+    with pytest.raises(ValueError):
+        O.orc_encode_query(np.zeros(8, np.float32))
+    x = np.ones(8, np.float32)
+    x[3] = np.nan
+    with pytest.raises(ValueError):
+        O.orc_encode_query(x)
+    x[3] = np.inf
+    with pytest.raises(ValueError):
+        O.orc_encode_query(x)
+
+
+@ref_only
+@pytest.mark.parametrize("dim", [4, 63, 64, 65, 100, 384, 768, 1023])
+def test_sm2_kernel_equals_reference_across_word_boundaries(dim):
+    # test_encoding.cpp:148-166 restated: 160 random pairs per dim
+    rng = np.random.Generator(np.random.PCG64(42 + dim))
+    for _ in range(160):
+        a = rng.standard_normal(dim).astype(np.float32)
+        b = rng.standard_normal(dim).astype(np.float32)
+        ca, ta = O.ref_encode_raw(a)
+        cb, tb = O.ref_encode_raw(b)
+        d = O.ref_sm2(ca, cb)
+        assert O.orc_sm2(ca, cb) == d == O.ref_sm2(cb, ca)
+        # pad bits zero (test_encoding.cpp:168-179)
+        W = O.words_for_dim(dim)
+        if dim % 64:
+            mask = np.uint64(~((1 << (dim % 64)) - 1) & 0xFFFFFFFFFFFFFFFF)
+            assert (ca[W - 1] & mask) == 0 and (ca[2 * W - 1] & mask) == 0
+
+
+@ref_only
+def test_dot4_bit_exact_with_reference():
+    rng = np.random.Generator(np.random.PCG64(1))
+    for d in (1, 3, 4, 7, 64, 99, 384, 768, 3072):
+        for _ in range(20):
+            a = rng.standard_normal(d).astype(np.float32)
+            b = rng.standard_normal(d).astype(np.float32)
+            assert O.orc_dot4(a, b).view(np.uint32) == O.ref_dot(a, b).view(np.uint32)
+
+
+@pytest.mark.parametrize("name", ["g1", "g2", "g3"])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_oracle_reproduces_golden(name, mode):
+    g = load_golden(name)
+    ix = O.OracleIndex(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    k = int(g["k"])
+    for ef in g["efs"]:
+        ef = int(ef)
+        r = ix.query_batch(g["queries"], ef, k, mode=mode, vslots=64, pools=True)
+        assert np.array_equal(r["ids"], g[f"ids_{ef}"])
+        assert np.array_equal(r["scores"].view(np.uint32), g[f"scores_{ef}"])
+        assert np.array_equal(r["count"], g[f"count_{ef}"])
+        assert np.array_equal(r["pool_n"], g[f"pool_n_{ef}"])
+        assert np.array_equal(r["pool_ids"], g[f"pool_ids_{ef}"])
+        assert np.array_equal(r["pool_dists"], g[f"pool_dists_{ef}"])
+        assert r["stats"]["tie_overflows"] == 0
+
+
+def test_oracle_float_topk_matches_golden_gt():
+    g = load_golden("g1")
+    gt = O.orc_float_topk(g["cold"], g["queries"], 10)
+    assert np.array_equal(gt, g["gt10"])
+
+
+@ref_only
+@pytest.mark.parametrize("sigma_mode", ["literal", "norm"])
+def test_sorted_list_formulation_equals_reference_fresh_graph(sigma_mode):
+    """SURVEY §8.A.3/4b on a fresh multi-threaded reference build: dual heap,
+    sorted list with exact visited, and sorted list with tiny lossy visited tables
+    all give the reference's ids, scores and pools."""
+    from paper_2605_02171_b200.datasets import mixture
+    base, q = mixture(6000, 128, 60, 0.35, seed=21, nq=150, sigma_mode=sigma_mode)
+    ref = O.RefIndex.build(base, m=8, ef_c=32, alpha=1.2, threads=4)
+    ix = O.OracleIndex.from_ref(ref)
+    for ef in (10, 16, 64, 128):
+        ids, sc, cnt = ref.run_query_batch(q, ef, 10, threads=4)
+        for mode, vs in ((0, 0), (1, 0), (2, 1024), (2, 32)):
+            r = ix.query_batch(q, ef, 10, mode=mode, vslots=vs)
+            assert np.array_equal(r["ids"], ids), (ef, mode, vs)
+            assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32))
+
+
+@ref_only
+def test_robust_prune_oracle_matches_reference():
+    g = load_golden("g1")
+    ref = O.RefIndex.from_parts(g["codes"], g["adj"], g["cold"], 64, int(g["m"]),
+                                int(g["entry"]))
+    ix = O.OracleIndex(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    rng = np.random.Generator(np.random.PCG64(3))
+    for _ in range(30):
+        ids = rng.choice(1500, 60, replace=False).astype(np.uint32)
+        dists = rng.integers(0, 200, 60).astype(np.uint32)
+        for alpha in (1.0, 1.2):
+            a = ref.robust_prune(ids, dists, 16, alpha)
+            b = ix.robust_prune(ids, dists, 16, alpha)
+            assert np.array_equal(a, b)
