@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native BQ query path (BASELINE.json metric):
+"batched QPS @ Recall@10 vs ef on 1 B200; gathered-bytes GB/s vs HBM peak".
+
+One step = one batch of `--nq` queries (default 10,000) through encode ->
+exact BQ beam search -> float32 rerank, on the headline workload (config 2:
+N=1e6, D=768, R=64, L=128, alpha=1.2, ef=64, k=10, literal sigma=0.3).
+The graph is the reference-built one cached in data_cache/ (see
+oracle/make_ref_graph.py); vectors and queries are regenerated (seeded).
+
+  value : device-resident queries, CUDA events on the launching stream around
+          each step, L2 flushed (256 MB write) between steps.
+  e2e   : the same search through the public API with pinned HOST buffers:
+          H2D of the queries and D2H of ids/scores/counts inside each step.
+  --impl reference : the reference's own CPU run_query_batch (oracle/_ref) on
+          the same graph/queries, all host threads.
+Multi-GPU (torchrun): replicas only — every rank runs its own batch on its own
+copy of the index; no collective on the data path; max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched QPS @ Recall@10 vs ef on 1 B200; gathered-bytes GB/s vs HBM peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ef", type=int, default=64)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--nq", type=int, default=10_000)
+    ap.add_argument("--n", type=int, default=None, help="override corpus size (testing)")
+    ap.add_argument("--sigma-mode", default="literal", choices=["literal", "norm"])
+    ap.add_argument("--sweep", default="auto", help="extra ef values ('auto', 'none', list)")
+    ap.add_argument("--sweep-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--recall-queries", type=int, default=1000)
+    ap.add_argument("--visited-slots", type=int, default=0)
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(*a, file=sys.stderr, flush=True)
+
+
+def load_workload(args):
+    from paper_2605_02171_b200 import datasets, graphs
+    cfg = datasets.CONFIGS[args.config]
+    t0 = time.time()
+    base, queries = datasets.config_data(cfg, n=args.n, nq=args.nq, sigma_mode=args.sigma_mode)
+    log(f"[bench] generated {base.shape} + {queries.shape} in {time.time() - t0:.1f}s")
+    g = graphs.load_graph(cfg, args.sigma_mode, base.shape[0], base, builder="ref")
+    provenance = "reference qivr::build_index (cached, data_cache/)"
+    if g is None:
+        g = graphs.load_graph(cfg, args.sigma_mode, base.shape[0], base, builder="gpu")
+        provenance = "GPU builder qvg_build (cached, data_cache/)"
+    if g is None:
+        import paper_2605_02171_b200 as Q
+        log("[bench] no cached graph: building on the GPU (qvg_build)")
+        t0 = time.time()
+        st = {}
+        ix = Q.GpuIndex.build(base, Q.BuildParams(m=cfg.m, ef_c=cfg.ef_c, alpha=cfg.alpha),
+                              stats=st)
+        _, adj, _ = ix.export()
+        g = dict(adj=adj, entry=np.uint32(ix.entry_point), build_seconds=time.time() - t0)
+        path = graphs.graph_path(cfg, args.sigma_mode, base.shape[0], builder="gpu")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        np.savez(path, adj=adj, entry=np.uint32(ix.entry_point), m=np.uint32(cfg.m),
+                 ef_c=np.uint32(cfg.ef_c), alpha=np.float32(cfg.alpha),
+                 digest=graphs.data_digest(base), build_seconds=np.float64(g["build_seconds"]))
+        provenance = "GPU builder qvg_build (built in this run)"
+        ix.close()
+    return cfg, base, queries, g["adj"], int(g["entry"]), provenance
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload_key):
+    """dram bytes per launch of the search kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    e = d.get(workload_key)
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), e.get("source")
+
+
+def algorithmic_bytes(st, W, D, k, nq):
+    """sum_exp(4+4 deg) + evals*16W + |pool|*4D + 4D + 8k per query."""
+    return (st["adjacency_bytes"] + st["dist_evals"] * 16 * W + st["cold_accesses"] * 4 * D +
+            nq * (4 * D + 8 * k))
+
+
+def recall_at_k(res, gt, k):
+    """eval.cpp:171-195"""
+    tot = 0.0
+    for r, g in zip(res, gt):
+        gs = set(int(x) for x in g[:k])
+        tot += sum(1 for x in r[:k] if int(x) in gs) / k
+    return tot / len(res)
+
+
+def gpu_ground_truth(base_dev, queries, k, torch):
+    """Exact-enough fp32 brute force on the GPU (torch matmul, TF32 off) for a
+    query sample — evaluation only, not on the measured path."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    q = torch.from_numpy(queries).cuda()
+    best_s = torch.full((q.shape[0], k), -2.0, device="cuda")
+    best_i = torch.zeros((q.shape[0], k), dtype=torch.int64, device="cuda")
+    for r0 in range(0, base_dev.shape[0], 131072):
+        s = q @ base_dev[r0:r0 + 131072].T
+        ts, ti = torch.topk(s, k, dim=1)
+        cs = torch.cat([best_s, ts], 1)
+        ci = torch.cat([best_i, ti + r0], 1)
+        best_s, o = torch.topk(cs, k, dim=1)
+        best_i = torch.gather(ci, 1, o)
+    return best_i.cpu().numpy()
+
+
+# ----------------------------------------------------------------------------
+def run_reference_search(args, cfg, base, queries, adj, entry, k, ef, budget_s=60.0,
+                         steps=None, warmup=0):
+    """The reference's CPU path: qivr::run_query_batch on the same graph."""
+    from oracle.oracle import RefIndex
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    ref = RefIndex.from_graph(base, adj, cfg.m, entry, cfg.alpha, threads=threads)
+    log(f"[bench] reference index (stage0 + cached graph) in {time.time() - t0:.1f}s")
+    # calibrate a bounded per-step sample
+    t0 = time.time()
+    ref.run_query_batch(queries[:256], ef, k, threads=threads)
+    est = 256 / max(time.time() - t0, 1e-6)
+    return ref, threads, est
+
+
+def ours(args):
+    import torch
+
+    import paper_2605_02171_b200 as Q
+    from paper_2605_02171_b200 import _native as N
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, base, queries, adj, entry, provenance = load_workload(args)
+    n, D = base.shape
+    k, ef = args.k, args.ef
+
+    t0 = time.time()
+    qn, codes, _ = Q.encode_queries(base, device=local)  # stage0: normalize + encode
+    ix = Q.GpuIndex.from_arrays(codes, adj, qn, entry, device=local)
+    del codes
+    log(f"[bench] index in HBM in {time.time() - t0:.1f}s (n={n}, D={D}, R={ix.max_degree})")
+    stream = torch.cuda.current_stream()
+    ix.set_stream(stream)
+    nq = queries.shape[0]
+    W = ix.W
+
+    # ---- untimed stats passes: exact visited (algorithmic counts) and default
+    ex = ix.search_ex(queries, k=k, ef=ef, exact_visited=True, pools=False)
+    lo = ix.search_ex(queries, k=k, ef=ef, visited_slots=args.visited_slots, pools=False)
+    assert np.array_equal(ex["ids"], lo["ids"]), "lossy-visited result differs from exact"
+    alg_bytes = algorithmic_bytes(ex["stats"], W, D, k, nq)
+
+    q_host = torch.from_numpy(queries).pin_memory()
+    q_dev = q_host.cuda()
+    ids_d = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    sc_d = torch.empty((nq, k), dtype=torch.float32, device="cuda")
+    cnt_d = torch.empty(nq, dtype=torch.int32, device="cuda")
+    st_d = torch.empty(nq, dtype=torch.int32, device="cuda")
+    ids_h = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    sc_h = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    cnt_h = torch.empty(nq, dtype=torch.int32).pin_memory()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    opts = N.qvg_search_opts(visited_slots=args.visited_slots, entry_point=N.SENTINEL,
+                             timing_only=1)
+    import ctypes as C
+
+    def step_dev(efv=ef):
+        st = N.qvg_stats()
+        rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr(), nq, k, efv, C.byref(opts),
+                                   ids_d.data_ptr(), sc_d.data_ptr(), cnt_d.data_ptr(),
+                                   st_d.data_ptr(), None, None, None, None, C.byref(st))
+        if rc:
+            raise RuntimeError(N.last_error())
+        return st
+
+    def step_e2e():
+        rc = N.lib().qvg_search(ix._h, q_host.data_ptr(), nq, k, ef, ids_h.data_ptr(),
+                                sc_h.data_ptr(), cnt_h.data_ptr(), None, None)
+        if rc:
+            raise RuntimeError(N.last_error())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, sampler=None):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        kern = []
+        barrier()
+        if sampler:
+            sampler.start()
+        for i in range(steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            r = fn()
+            ev[i][1].record(stream)
+            if r is not None:
+                kern.append(r.search_ms)
+        barrier()
+        clocks = sampler.stop() if sampler else None
+        ms = [a.elapsed_time(b) for a, b in ev]
+        tot = sum(ms)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([tot], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        return tot, ms, kern, clocks
+
+    for _ in range(max(args.warmup, 3)):
+        step_dev()
+        step_e2e()
+    sampler = ClockSampler(local)
+    tot_ms, ms, kern_ms, clocks = timed(step_dev, args.steps, sampler)
+    e2e_ms, _, _, _ = timed(step_e2e, args.steps)
+    ids = ids_d.cpu().numpy().view(np.uint32)
+    assert np.array_equal(ids, ex["ids"]), "timed results differ from the stats pass"
+
+    value = world * nq * args.steps / (tot_ms / 1e3)
+    e2e = world * nq * args.steps / (e2e_ms / 1e3)
+    kern_avg = float(np.mean(kern_ms))
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (kern_avg / 1e3) / 1e9
+    key = f"cfg{args.config}_{args.sigma_mode}_ef{ef}_nq{nq}"
+    traffic, traffic_src = ncu_traffic(key)
+
+    # ---- recall (GPU fp32 brute force on a sample) ---------------------------
+    rq = min(args.recall_queries, nq)
+    base_dev = torch.from_numpy(qn).cuda()
+    qnq, _, _ = Q.encode_queries(queries[:rq], device=local)  # normalised like query()
+    gt = gpu_ground_truth(base_dev, qnq, k, torch)
+    del base_dev
+    recall = recall_at_k(ex["ids"][:rq], gt, k)
+
+    # ---- ef sweep ------------------------------------------------------------
+    sweep = []
+    efs = [] if args.sweep == "none" else (
+        [e for e in cfg.efs if e != ef] if args.sweep == "auto" else
+        [int(x) for x in args.sweep.split(",") if x])
+    for e in efs:
+        if e < k:
+            continue
+        s_ex = ix.search_ex(queries, k=k, ef=e, exact_visited=True, pools=False)
+        for _ in range(3):
+            step_dev(e)
+        t_ms, _, km, _ = timed(lambda: step_dev(e), args.sweep_steps)
+        b = algorithmic_bytes(s_ex["stats"], W, D, k, nq)
+        ka = float(np.mean(km))
+        sweep.append(dict(ef=e, qps=world * nq * args.sweep_steps / (t_ms / 1e3),
+                          recall_at_10=recall_at_k(s_ex["ids"][:rq], gt, k),
+                          kernel_ms=ka, gbs=b / (ka / 1e3) / 1e9,
+                          frac=b / (ka / 1e3) / 1e9 / peak,
+                          bytes_per_query=b / nq,
+                          expansions_per_query=s_ex["stats"]["expansions"] / nq,
+                          evals_per_query=s_ex["stats"]["dist_evals"] / nq))
+
+    # ---- CPU baseline + full-size parity (rank 0, N=1) ------------------------
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import ref_available
+            if ref_available():
+                ref, threads, est = run_reference_search(args, cfg, base, queries, adj, entry,
+                                                         k, ef)
+                runs = []
+                for _ in range(3):
+                    t0 = time.time()
+                    rids, rsc, rcnt = ref.run_query_batch(queries, ef, k, threads=threads)
+                    runs.append(nq / (time.time() - t0))
+                t0 = time.time()
+                n1 = 300
+                ref.run_query_batch(queries[:n1], ef, k, threads=1)
+                qps1 = n1 / (time.time() - t0)
+                cpu = {"value": float(np.mean(runs)), "unit": "queries/s", "cores": threads,
+                       "kind": "reference",
+                       "sample": f"{nq} cfg{args.config} queries x 3 runs, ef={ef}, k={k}, "
+                                 f"qivr::run_query_batch with {threads} threads "
+                                 "(oracle/_ref, -O3 -march=sapphirerapids)",
+                       "qps_1thread": qps1, "cpu": cpu_model()}
+                sc_ours = ex["scores"].view(np.uint32)
+                parity = {"queries": nq,
+                          "ids_identical": float((rids == ex["ids"]).all(axis=1).mean()),
+                          "scores_bit_identical": float(
+                              (rsc.view(np.uint32) == sc_ours).all(axis=1).mean()),
+                          "vs": "reference run_query_batch on the same graph"}
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "error": str(exc)[:200]}
+
+    if rank != 0:
+        return
+    out = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded clustered mixture)",
+        "config": {"workload": f"cfg{args.config}: N={n} D={D} R={ix.max_degree} "
+                               f"L={cfg.ef_c} alpha={cfg.alpha} nq={nq} ef={ef} k={k} "
+                               f"sigma={cfg.sigma} ({args.sigma_mode})",
+                   "graph": provenance, "l2": "flushed between steps (256 MB write)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "recall_at_10": recall, "recall_gt": f"fp32 brute force, {rq} queries"},
+        "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * D * 4,
+                "d2h_bytes_per_step": nq * (8 * k + 4) + 4},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "search_kernel (fused BQ beam search + rerank)",
+                     "kernel_ms": kern_avg, "kernel_share": sum(kern_ms) / tot_ms,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_query": alg_bytes / nq, "peak_source": peak_src,
+                     "traffic_source": traffic_src},
+        "counters": {"expansions_per_query": ex["stats"]["expansions"] / nq,
+                     "tie_expansions_per_query": ex["stats"]["tie_expansions"] / nq,
+                     "evals_per_query_exact": ex["stats"]["dist_evals"] / nq,
+                     "evals_per_query_lossy": lo["stats"]["dist_evals"] / nq,
+                     "tie_overflows": ex["stats"]["tie_overflows"]},
+        "cpu_baseline": cpu, "parity": parity, "ef_sweep": sweep,
+        "gpu_launches": 2 * args.steps, "clocks": clocks,
+    }
+    line = json.dumps(out)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(line + "\n")
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    cfg, base, queries, adj, entry, provenance = load_workload(args)
+    k, ef = args.k, args.ef
+    ref, threads, est = run_reference_search(args, cfg, base, queries, adj, entry, k, ef)
+    total = args.steps + max(args.warmup, 0)
+    per = int(max(64, min(queries.shape[0], 90.0 * est / max(total, 1))))
+    log(f"[bench] reference: ~{est:.0f} q/s, {per} queries per step")
+    for i in range(args.warmup):
+        ref.run_query_batch(queries[:per], ef, k, threads=threads)
+    t = 0.0
+    for i in range(args.steps):
+        off = (i * per) % max(1, queries.shape[0] - per + 1)
+        t0 = time.time()
+        ref.run_query_batch(queries[off:off + per], ef, k, threads=threads)
+        t += time.time() - t0
+    value = per * args.steps / t
+    n, D = base.shape
+    out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic (seeded clustered mixture)", "impl": "reference",
+           "config": {"workload": f"cfg{args.config}: N={n} D={D} R={2 * cfg.m} "
+                                  f"L={cfg.ef_c} alpha={cfg.alpha} nq={queries.shape[0]} "
+                                  f"ef={ef} k={k} sigma={cfg.sigma} ({args.sigma_mode})",
+                      "graph": provenance},
+           "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
+                            "kind": "reference",
+                            "sample": f"{per} queries per step (bounded sample of the "
+                                      f"{queries.shape[0]}-query batch), qivr::run_query_batch",
+                            "cpu": cpu_model()},
+           "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -100,7 +100,8 @@ typedef struct qvg_search_opts {
     uint32_t exact_visited; /* 1: exact global visited bitmap (stats / validation)   */
     uint32_t entry_point;   /* UINT32_MAX: the index's entry point                   */
     uint32_t no_rerank;     /* 1: skip rerank (pool only)                            */
-    uint32_t reserved[3];
+    uint32_t timing_only;   /* 1: stats carries device timings only (no counter D2H)  */
+    uint32_t reserved[2];
 } qvg_search_opts;
 
 const char* qvg_last_error(void);

@@ -79,6 +79,8 @@ def _ref_lib():
                                         _u32p, C.POINTER(C.c_uint32)]
         L.qref_from_parts.argtypes = [_u64p, _u32p, _f32p, C.c_uint64, C.c_uint32, C.c_uint32,
                                       C.c_uint32, C.c_float, C.POINTER(vp)]
+        L.qref_index_from_graph.argtypes = [_f32p, C.c_uint64, C.c_uint32, _u32p, C.c_uint32,
+                                            C.c_uint32, C.c_float, C.c_uint32, C.POINTER(vp)]
         _ref = L
     return _ref
 
@@ -145,6 +147,17 @@ class RefIndex:
         h = C.c_void_p()
         _ref_check(_ref_lib().qref_from_parts(codes, adj, cold, n, dim, m, entry, alpha,
                                               C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_graph(cls, data, adj, m, entry, alpha=1.2, threads=None):
+        """stage0_preinstall(data) + the given adjacency / entry point."""
+        data = np.ascontiguousarray(data, dtype=np.float32)
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        h = C.c_void_p()
+        _ref_check(_ref_lib().qref_index_from_graph(data, data.shape[0], data.shape[1], adj, m,
+                                                    entry, alpha, threads or os.cpu_count() or 1,
+                                                    C.byref(h)))
         return cls(h)
 
     def save(self, path):

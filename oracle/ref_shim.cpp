@@ -243,4 +243,25 @@ int qref_from_parts(const uint64_t* codes, const uint32_t* adj, const float* col
     });
 }
 
+// Reference Index over raw (unnormalised) vectors and a given graph: the
+// reference's own stage0_preinstall (builder.cpp:59-88: normalize_l2 +
+// SignatureStore::encode per row, bulk adjacency, medoid entry) followed by
+// installing the given adjacency slots and entry point.  Used to run the
+// reference search on a cached graph without repeating the build.
+int qref_index_from_graph(const float* data, uint64_t n, uint32_t dim, const uint32_t* adj,
+                          uint32_t m, uint32_t entry, float alpha, uint32_t threads,
+                          void** out) {
+    *out = nullptr;
+    return guarded([&] {
+        qivr::BuildParams p;
+        p.m = m;
+        p.alpha = alpha;
+        p.threads = threads;
+        auto ix = std::make_unique<qivr::Index>(qivr::stage0_preinstall(data, n, dim, p));
+        std::memcpy(ix->adjacency.raw(), adj, ix->adjacency.size_bytes());
+        ix->entry_point = entry;
+        *out = ix.release();
+    });
+}
+
 }  // extern "C"

@@ -153,7 +153,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     tcap = (tcap + 3) & ~3u;
     const bool exact = opts && opts->exact_visited;
     const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
-    const bool want_ctr = stats != nullptr || out_qctr != nullptr;
+    const bool want_ctr = out_qctr != nullptr || (stats && !(opts && opts->timing_only));
 
     qvg_status st = QVG_OK;
     // ---- inputs -------------------------------------------------------------
@@ -206,6 +206,8 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     }
 
     // ---- pipeline -------------------------------------------------------------
+    uint32_t* d_flags = reinterpret_cast<uint32_t*>(static_cast<char*>(h->s_counter.p) + 32);
+    a.flags = d_flags;
     cudaEventRecord(h->ev[0], s);
     const void* din = user_in;
     if (!in_dev) {
@@ -213,12 +215,12 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         if (e != cudaSuccess) return cuda_status(e, "H2D(queries)");
         din = h->s_in.p;
     }
-    cudaMemsetAsync(h->s_counter.p, 0, 64, s);
+    cudaMemsetAsync(h->s_counter.p, 0, 64, s);  // work counter + flag word
     cudaEventRecord(h->ev[1], s);
     if (mode.encode) {
         launch_encode(static_cast<const float*>(din), nq, ix.dim, ix.Dp,
                       static_cast<float*>(h->s_qn.p), static_cast<uint4*>(h->s_qc.p), nullptr,
-                      static_cast<int32_t*>(h->s_qst.p), s);
+                      static_cast<int32_t*>(h->s_qst.p), d_flags, s);
     } else {
         launch_codes_to_chunks(static_cast<const uint64_t*>(din), nq, ix.W,
                                static_cast<uint4*>(h->s_qc.p), s);
@@ -234,19 +236,13 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
             if (e != cudaSuccess) return cuda_status(e, "D2H(results)");
         }
     }
-    // status summary (copied even when the caller did not ask for statuses)
-    std::vector<int32_t> qst_host;
-    int32_t* qst_view = nullptr;
-    if (o_st.copy_back) {
-        qst_view = out_query_status;
-    } else {
-        qst_host.resize(nq);
-        e = cudaMemcpyAsync(qst_host.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
-        qst_view = qst_host.data();
-    }
+    // 4-byte summary of all per-query statuses
+    uint32_t hflags = 0;
+    e = cudaMemcpyAsync(&hflags, d_flags, 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_status(e, "D2H(flags)");
+    const bool counters = out_qctr != nullptr || (stats && !(opts && opts->timing_only));
     std::vector<uint32_t> ctr_host;
-    if (stats && !o_ctr.copy_back) {
+    if (stats && counters && !o_ctr.copy_back) {
         ctr_host.resize(nq * 8);
         e = cudaMemcpyAsync(ctr_host.data(), o_ctr.dev, nq * 32, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_status(e, "D2H(counters)");
@@ -267,32 +263,38 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         stats->device_ms = t;
         cudaEventElapsedTime(&t, h->ev[0], h->ev[4]);
         stats->total_ms = t;
-        const uint32_t* c = o_ctr.copy_back ? out_qctr : ctr_host.data();
         stats->queries = nq;
-        for (uint64_t i = 0; i < nq; ++i) {
-            const uint32_t* r = c + i * 8;
-            if (r[7] == QVG_Q_NONFINITE_COORD || r[7] == QVG_Q_BAD_NORM ||
-                r[7] == QVG_Q_NONFINITE_CODE)
-                continue;
-            stats->expansions += r[0];
-            stats->tie_expansions += r[1];
-            stats->dist_evals += r[2];
-            stats->inpool_drops += r[3];
-            stats->adjacency_slots += r[4];
-            stats->cold_accesses += do_rerank ? r[5] : 0;
-            stats->tie_overflows += r[7] == QVG_Q_TIE_OVERFLOW;
-            if (r[6] > stats->max_tie_depth) stats->max_tie_depth = r[6];
-            stats->adjacency_bytes += 4ull * r[0] + 4ull * r[4];
+        if (counters) {
+            const uint32_t* c = o_ctr.copy_back ? out_qctr : ctr_host.data();
+            for (uint64_t i = 0; i < nq; ++i) {
+                const uint32_t* r = c + i * 8;
+                if (r[7] == QVG_Q_NONFINITE_COORD || r[7] == QVG_Q_BAD_NORM ||
+                    r[7] == QVG_Q_NONFINITE_CODE)
+                    continue;
+                stats->expansions += r[0];
+                stats->tie_expansions += r[1];
+                stats->dist_evals += r[2];
+                stats->inpool_drops += r[3];
+                stats->adjacency_slots += r[4];
+                stats->cold_accesses += do_rerank ? r[5] : 0;
+                stats->tie_overflows += r[7] == QVG_Q_TIE_OVERFLOW;
+                if (r[6] > stats->max_tie_depth) stats->max_tie_depth = r[6];
+                stats->adjacency_bytes += 4ull * r[0] + 4ull * r[4];
+            }
+            stats->code_bytes = stats->dist_evals * 16ull * ix.W;
+            stats->rerank_bytes = stats->cold_accesses * 4ull * ix.dim;
+            stats->io_bytes = nq * (4ull * ix.dim + (do_rerank ? 8ull * k : 0));
         }
-        stats->code_bytes = stats->dist_evals * 16ull * ix.W;
-        stats->rerank_bytes = stats->cold_accesses * 4ull * ix.dim;
-        stats->io_bytes = nq * (4ull * ix.dim + (do_rerank ? 8ull * k : 0));
     }
-    // overall status: first invalid query (the reference's single-threaded
-    // batch throws at the first one), else tie overflow
+    if (hflags == 0) return QVG_OK;
+    // rare path: locate the first offending query (the reference's
+    // single-threaded batch throws at the first invalid one)
+    std::vector<int32_t> qs(nq);
+    e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
     int64_t first_bad = -1, first_ovf = -1;
     for (uint64_t i = 0; i < nq; ++i) {
-        const int32_t v = qst_view[i];
+        const int32_t v = qs[i];
         if (v == QVG_Q_TIE_OVERFLOW) {
             if (first_ovf < 0) first_ovf = (int64_t)i;
         } else if (v != 0 && first_bad < 0) {
@@ -300,7 +302,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         }
     }
     if (first_bad >= 0) {
-        set_error(std::string(qstatus_message(qst_view[first_bad])) + " (query " +
+        set_error(std::string(qstatus_message(qs[first_bad])) + " (query " +
                   std::to_string(first_bad) + ")");
         return QVG_INVALID_ARGUMENT;
     }
@@ -386,7 +388,7 @@ qvg_status qvg_encode(int device, const float* x, uint64_t nq, uint32_t dim,
     if (e == cudaSuccess) {
         launch_encode(static_cast<const float*>(d_x), nq, dim, Dp, static_cast<float*>(d_qn),
                       static_cast<uint4*>(d_qc), static_cast<float*>(d_tau),
-                      static_cast<int32_t*>(d_st), 0);
+                      static_cast<int32_t*>(d_st), nullptr, 0);
         launch_chunks_to_codes(static_cast<const uint4*>(d_qc), nq, W,
                                static_cast<uint64_t*>(d_codes), 0);
         e = cudaGetLastError();

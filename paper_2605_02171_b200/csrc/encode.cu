@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ x
                                                      float* __restrict__ qn,
                                                      uint4* __restrict__ qcodes,
                                                      float* __restrict__ tau_out,
-                                                     int32_t* __restrict__ status) {
+                                                     int32_t* __restrict__ status,
+                                                     uint32_t* __restrict__ flags) {
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (q >= nq) return;
     const uint32_t W = (dim + 63) / 64;
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ x
     if (st == QVG_Q_OK && (!(norm > 0.0) || isinf(norm))) st = QVG_Q_BAD_NORM;
     if (st != QVG_Q_OK) {
         status[q] = st;
+        if (flags) atomicOr(flags, 1u << st);
         if (tau_out) tau_out[q] = 0.0f;
         for (uint32_t i = 0; i < Dp; ++i) out[i] = 0.0f;
         for (uint32_t w = 0; w < W; ++w) code[w] = make_uint4(0, 0, 0, 0);
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ x
     for (uint32_t i = dim; i < Dp; ++i) out[i] = 0.0f;
     if (!yfinite) {
         status[q] = QVG_Q_NONFINITE_CODE;
+        if (flags) atomicOr(flags, 1u << QVG_Q_NONFINITE_CODE);
         if (tau_out) tau_out[q] = 0.0f;
         for (uint32_t w = 0; w < W; ++w) code[w] = make_uint4(0, 0, 0, 0);
         return;
@@ -152,14 +155,15 @@ __global__ void chunks_to_codes_kernel(const uint4* __restrict__ in, uint64_t ro
 }  // namespace
 
 void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float* qn,
-                   uint4* qcodes, float* tau, int32_t* status, cudaStream_t s) {
+                   uint4* qcodes, float* tau, int32_t* status, uint32_t* flags,
+                   cudaStream_t s) {
     if (nq == 0) return;
     const unsigned blocks = (unsigned)((nq + 127) / 128);
     const bool vec4 = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     if (vec4)
-        encode_kernel<true><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status);
+        encode_kernel<true><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
     else
-        encode_kernel<false><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status);
+        encode_kernel<false><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
 }
 
 void launch_codes_to_chunks(const uint64_t* ref_codes, uint64_t rows, uint32_t W, uint4* out,

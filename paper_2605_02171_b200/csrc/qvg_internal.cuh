@@ -59,8 +59,9 @@ qvg_status grow(Buffer& b, size_t bytes);
 bool is_device_ptr(const void* p);
 
 // kernels (encode.cu / search.cu)
+// flags (nullable): atomicOr(1 << status) for every rejected query
 void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float* qn,
-                   uint4* qcodes, float* tau, int32_t* status, cudaStream_t s);
+                   uint4* qcodes, float* tau, int32_t* status, uint32_t* flags, cudaStream_t s);
 void launch_codes_to_chunks(const uint64_t* ref_codes, uint64_t rows, uint32_t W, uint4* out,
                             cudaStream_t s);
 void launch_chunks_to_codes(const uint4* chunks, uint64_t rows, uint32_t W, uint64_t* out,
@@ -84,6 +85,7 @@ struct SearchLaunch {
     uint32_t* pool_n;
     uint32_t* qctr;
     unsigned long long* counter;
+    uint32_t* flags;        // atomicOr(1 << QVG_Q_TIE_OVERFLOW) on overflow
     uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
     uint64_t exact_words;   // words per slot
 };

@@ -516,6 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             if (lane == 0) a.pool_n[q] = np;
         }
         const int32_t qstatus = overflow ? QVG_Q_TIE_OVERFLOW : QVG_Q_OK;
+        if (lane == 0 && overflow && a.flags) atomicOr(a.flags, 1u << QVG_Q_TIE_OVERFLOW);
         if (lane == 0) {
             if (a.out_status) a.out_status[q] = qstatus;
             if (a.qctr) {

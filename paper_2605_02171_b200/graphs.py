@@ -1,0 +1,44 @@
+"""Cached graph inputs for the benchmark configs.
+
+A cached graph is the adjacency (reference slot layout, n x (2m+1) u32) and
+entry point of an index over the seeded dataset of a config; the vectors are
+regenerated (datasets.py) and verified against the stored digest, and the codes
+are re-encoded on the GPU (stage0: normalise + encode_sm2).  Files live in
+data_cache/ (git-ignored, shipped with the working tree).
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+
+from .datasets import Config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CACHE = os.environ.get("QVG_DATA_CACHE", os.path.join(ROOT, "data_cache"))
+
+
+def data_digest(base: np.ndarray) -> str:
+    """sha256 over a strided sample of rows plus the shape (cheap at 1M x 3072)."""
+    h = hashlib.sha256()
+    h.update(np.array(base.shape, np.int64).tobytes())
+    step = max(1, base.shape[0] // 4096)
+    h.update(np.ascontiguousarray(base[::step]).tobytes())
+    h.update(np.ascontiguousarray(base[-1]).tobytes())
+    return h.hexdigest()[:32]
+
+
+def graph_path(cfg: Config, sigma_mode: str, n: int, builder: str = "ref") -> str:
+    return os.path.join(CACHE, f"{cfg.name}_{sigma_mode}_n{n}_{builder}.npz")
+
+
+def load_graph(cfg: Config, sigma_mode: str, n: int, base: np.ndarray, builder="ref"):
+    """-> dict(adj, entry, ...) or None if absent / stale."""
+    p = graph_path(cfg, sigma_mode, n, builder)
+    if not os.path.exists(p):
+        return None
+    g = dict(np.load(p))
+    if str(g["digest"]) != data_digest(base):
+        return None
+    return g
