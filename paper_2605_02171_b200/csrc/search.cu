@@ -3,7 +3,7 @@
 //
 // Reference behaviour reproduced (paths under /root/reference/proj/core):
 //   beam_search_words  search.cpp:27-81   dual-heap best-first search
-//   candidate_less     graph.hpp:28-30    (dist, id) order == u64 key order
+//   candidate_less     graph.hpp:28-30    (dist, id) order == key order
 //   sm2_distance_words encoding.hpp:169-176
 //   rerank             search.cpp:96-120  4-chain double dot (vec_math.hpp:13-26),
 //                                         sort (score desc, id asc), take k
@@ -11,22 +11,24 @@
 // The dual heap is replaced by the equivalent sorted-list state machine of
 // SURVEY §8.A.3 (validated against the reference: tests/test_oracle_pins.py and
 // the GPU parity tests):
-//   P   sorted pool of <= ef u64 keys (dist<<32 | id) + expanded flags (smem,
-//       double-buffered)
+//   P   sorted pool of <= ef keys in shared memory.  key = dist<<33 | exp<<32 | id;
+//       the order ignores the `exp` (expanded) bit, so (dist, id) order is a
+//       plain u64 compare of (key & ~EXP).
 //   T   tie stack: keys evicted from P while unexpanded whose dist equals the
-//       pool's worst dist.  Worst dist never increases once P is full, so every
-//       live T entry shares one dist (tdist) and new entries (always smaller
-//       keys) are pushed on top; a drop of the worst dist kills all of T.
-//   vis lossy direct-mapped visited table (smem).  A forgotten node that is
-//       scored again is either already in P (found by exact lookup, dropped) or
-//       has key > max(P) and is rejected, so results are unchanged
-//       (SURVEY §8.A.4b); misses cost only bandwidth.
+//       pool's worst dist.  The worst dist never increases once P is full, so
+//       all live T entries share one dist (tdist) and new entries (always
+//       smaller keys) are pushed on top; a drop of the worst dist kills all of T.
+//   vis lossy direct-mapped visited table.  A forgotten node that is scored
+//       again is either already in P (exact lookup, dropped) or has key > max(P)
+//       and is rejected, so results are unchanged; misses only
+//       cost bandwidth.
 // Admission of a row is the exact parallel form of the sequential loop: the
 // i-th surviving neighbour c_i is admitted iff
 //   #{p in P : p < c_i} + #{j < i : c_j < c_i} < ef
 // and P' = first ef of merge(P, admitted).  Only "contenders" (c < max(P), or
-// any c while P is not full) can matter, so the per-row sort/merge work scales
-// with the few contenders, not with the row length.
+// any c while P is not full) can matter, so after the gather only contenders
+// (a handful per row once P is full) are ranked and merged; the merge moves
+// only the tail of P at and after the first insertion point, in place.
 #include <cuda_runtime.h>
 
 #include "qvg_internal.cuh"
@@ -36,7 +38,14 @@ namespace qvg {
 namespace {
 
 constexpr uint64_t kInfKey = ~0ull;
+constexpr uint64_t kExp = 1ull << 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint64_t mkkey(uint32_t dist, uint32_t id) {
+    return ((uint64_t)dist << 33) | id;
+}
+__device__ __forceinline__ uint64_t ordk(uint64_t k) { return k & ~kExp; }
+__device__ __forceinline__ uint32_t kdist(uint64_t k) { return (uint32_t)(k >> 33); }
 
 __device__ __forceinline__ uint32_t vhash(uint32_t id, uint32_t lg) {
     return (id * 0x9E3779B1u) >> (32 - lg);
@@ -59,11 +68,23 @@ __device__ __forceinline__ uint4 ldg_chunk(const uint4* p) {
     return r;
 }
 
-__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t n, uint64_t x) {
+// first index i in [0, n) with ordk(a[i]) >= x
+__device__ __forceinline__ uint32_t lower_bound_key(const uint64_t* a, uint32_t n, uint64_t x) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1;
+        if (ordk(a[mid]) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// #{j < m : a[j] <= x} for non-decreasing a
+__device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t m, uint32_t x) {
+    uint32_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -104,7 +125,7 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
 }
 
 struct SmemLayout {
-    uint32_t pk0, pk1, cand, ctd, cid, stg, pf0, pf1, qc, tie, vis, misc, total;
+    uint32_t pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, total;
 };
 
 // Per-warp shared-memory carve-up (bytes, every region 16-B aligned).
@@ -117,98 +138,56 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
         o += (bytes + 15u) & ~15u;
         return at;
     };
-    L.pk0 = take(8 * EFM);
-    L.pk1 = take(8 * EFM);
-    L.cand = take(8 * RM);  // candidate keys in row order; later sorted contenders
-    L.ctd = take(8 * RM);   // contenders in row order; later evicted keys
-    L.cid = take(4 * RM);   // compacted row ids; later eviction flags
+    L.pk = take(8 * EFM);   // pool keys
+    L.ctd = take(8 * RM);   // contenders, row order
+    L.evk = take(8 * RM);   // keys evicted this step, by (newpos - ef)
+    L.crp = take(4 * RM);   // contender rank in P, row order
+    L.csrp = take(4 * RM);  // contender rank in P, key order
+    L.cid = take(4 * RM);   // compacted row ids to score
     L.stg = take(4 * RM);   // tie-stack additions, ascending
-    L.pf0 = take(EFM);
-    L.pf1 = take(EFM);
-    L.qc = take(16 * W);
+    L.qc = take(16 * W);    // query code chunks
     L.tie = take(4 * tie_cap);
     L.vis = take(4 * vis_slots);  // rerank scores alias this region (vis_slots >= EFM)
-    L.misc = take(16);
     L.total = o;
     return L;
 }
 
-template <int EFW, int RW, int PB>
+// G lanes score one code row; CPL = chunks per lane (W == G*CPL), or CPL == 0
+// for the generic path (runtime W and G, groups of 3 chunks per lane).
+template <int RW, int G, int CPL, int PB>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    search_kernel(const SearchLaunch a, const uint32_t warp_bytes, const uint32_t G) {
+    search_kernel(const SearchLaunch a, const uint32_t warp_bytes, const uint32_t Grt) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr uint32_t EFM = EFW * 32;
     constexpr uint32_t RM = RW * 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const DevIndex ix = a.ix;
-    const uint32_t W = ix.W;
+    const uint32_t W = CPL ? (uint32_t)(G * CPL) : ix.W;
     const uint32_t VS = 1u << a.vis_log2;
+    const uint32_t ef = a.ef;
+    const uint32_t EFM = (ef + 31u) & ~31u;
     const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
-    uint64_t* pk = reinterpret_cast<uint64_t*>(base + L.pk0);
-    uint64_t* pk2 = reinterpret_cast<uint64_t*>(base + L.pk1);
-    uint8_t* pf = base + L.pf0;
-    uint8_t* pf2 = base + L.pf1;
-    uint64_t* cand = reinterpret_cast<uint64_t*>(base + L.cand);
-    uint64_t* cs = cand;  // alias: sorted contenders
+    uint64_t* pk = reinterpret_cast<uint64_t*>(base + L.pk);
     uint64_t* ctd = reinterpret_cast<uint64_t*>(base + L.ctd);
-    uint64_t* evk = ctd;  // alias: evicted keys by (newpos - ef)
+    uint64_t* evk = reinterpret_cast<uint64_t*>(base + L.evk);
+    uint32_t* crp = reinterpret_cast<uint32_t*>(base + L.crp);
+    uint32_t* csrp = reinterpret_cast<uint32_t*>(base + L.csrp);
     uint32_t* cid = reinterpret_cast<uint32_t*>(base + L.cid);
-    uint8_t* evf = reinterpret_cast<uint8_t*>(base + L.cid);  // alias: eviction flags
+    uint32_t* stg = reinterpret_cast<uint32_t*>(base + L.stg);
     uint4* qc = reinterpret_cast<uint4*>(base + L.qc);
     uint32_t* tie = reinterpret_cast<uint32_t*>(base + L.tie);
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
 
-    const uint32_t ef = a.ef;
-    const uint32_t RPP = 32u / G;  // code rows per pass
-    const uint32_t sub = lane & (G - 1u);
-    const uint32_t grp = lane / G;
-    const uint32_t cpl = (W + G - 1u) / G;
+    const uint32_t g_ = CPL ? (uint32_t)G : Grt;  // lanes per code row
+    const uint32_t RPP = 32u / g_;                 // code rows per pass
+    const uint32_t sub = lane & (g_ - 1u);
+    const uint32_t grp = lane / g_;
+    const uint32_t cpl = CPL ? (uint32_t)CPL : (W + g_ - 1u) / g_;
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     uint32_t* xbits = a.exact_bits ? a.exact_bits + gwarp * a.exact_words : nullptr;
-
-    // Score the n compacted ids in cid[0..n) into cand[0..n) (row order).
-    auto gather = [&](uint32_t n) {
-        for (uint32_t b0 = 0; b0 < n; b0 += RPP * PB) {
-            uint32_t acc[PB];
-#pragma unroll
-            for (int b = 0; b < PB; ++b) acc[b] = 0;
-            for (uint32_t c0 = 0; c0 < cpl; c0 += 3) {
-                uint4 qv[3];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const uint32_t w = sub + (c0 + c) * G;
-                    qv[c] = (c0 + c < cpl && w < W) ? qc[w] : make_uint4(0, 0, 0, 0);
-                }
-                uint4 buf[PB][3];
-#pragma unroll
-                for (int b = 0; b < PB; ++b) {
-                    const uint32_t r = b0 + b * RPP + grp;
-                    const uint32_t id = r < n ? cid[r] : 0u;
-                    const uint4* row = ix.codes + (size_t)id * W;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const uint32_t w = sub + (c0 + c) * G;
-                        buf[b][c] = (r < n && c0 + c < cpl && w < W) ? ldg_chunk(row + w) : qv[c];
-                    }
-                }
-#pragma unroll
-                for (int b = 0; b < PB; ++b)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[b] += sm2_chunk(qv[c], buf[b][c]);
-            }
-#pragma unroll
-            for (int b = 0; b < PB; ++b) {
-                for (uint32_t off = G >> 1; off > 0; off >>= 1)
-                    acc[b] += __shfl_xor_sync(kFull, acc[b], off);
-                const uint32_t r = b0 + b * RPP + grp;
-                if (sub == 0 && r < n) cand[r] = ((uint64_t)acc[b] << 32) | cid[r];
-            }
-        }
-    };
 
     for (;;) {
         unsigned long long qq = 0;
@@ -247,55 +226,231 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         } else {
             for (uint32_t i = lane; i < VS; i += 32) vis[i] = kSentinel;
         }
-        uint32_t entry = a.entry;
+        const uint32_t entry = a.entry;
         if (lane == 0) {
-            cid[0] = entry;
             if (xbits) atomicOr(xbits + (entry >> 5), 1u << (entry & 31));
             else vis[vhash(entry, a.vis_log2)] = entry;
         }
-        __syncwarp();
-        gather(1);
-        __syncwarp();
-        if (lane == 0) {
-            pk[0] = cand[0];
-            pf[0] = 0;
-        }
-        __syncwarp();
-        uint32_t np = 1, tn = 0, tdist = 0;
-        uint32_t c_exp = 0, c_tie = 0, c_eval = 1, c_drop = 0, c_slots = 0, c_maxtie = 0;
+        uint32_t np = 0, tn = 0, tdist = 0, hint = 0;
+        uint32_t c_exp = 0, c_tie = 0, c_eval = 0, c_drop = 0, c_slots = 0, c_maxtie = 0;
         bool overflow = false;
+        uint32_t n = 1;  // rows to score in cid[0..n)
+        if (lane == 0) cid[0] = entry;
+        __syncwarp();
 
-        // ---- best-first loop ----------------------------------------------------
+        // ---- best-first loop (iteration 0 scores the entry point) --------------
         for (;;) {
-            // 1. pick: first unexpanded pool entry, else the top of the tie stack
-            int pick = -1;
+            c_eval += n;
+            // (a) gather code rows + SM2 distances; contenders -> ctd / crp
+            const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
+            uint32_t m = 0;
+            for (uint32_t b0 = 0; b0 < n; b0 += RPP * PB) {
+                uint32_t acc[PB];
+                uint32_t rid[PB];
 #pragma unroll
-            for (int e = 0; e < EFW; ++e) {
-                const uint32_t idx = lane + 32u * e;
-                const bool un = idx < np && pf[idx] == 0;
+                for (int b = 0; b < PB; ++b) {
+                    acc[b] = 0;
+                    const uint32_t r = b0 + b * RPP + grp;
+                    rid[b] = r < n ? cid[r] : kSentinel;
+                }
+                if (CPL) {
+                    uint4 qv[CPL > 0 ? CPL : 1];
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) qv[c] = qc[sub + c * G];
+                    uint4 buf[PB][CPL > 0 ? CPL : 1];
+#pragma unroll
+                    for (int b = 0; b < PB; ++b) {
+                        const uint4* row = ix.codes + (size_t)rid[b] * W + sub;
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c)
+                            buf[b][c] = rid[b] != kSentinel ? ldg_chunk(row + c * G) : qv[c];
+                    }
+#pragma unroll
+                    for (int b = 0; b < PB; ++b)
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) acc[b] += sm2_chunk(qv[c], buf[b][c]);
+                } else {
+                    for (uint32_t c0 = 0; c0 < cpl; c0 += 3) {
+                        uint4 qv[3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const uint32_t w = sub + (c0 + c) * g_;
+                            qv[c] = (c0 + c < cpl && w < W) ? qc[w] : make_uint4(0, 0, 0, 0);
+                        }
+                        uint4 buf[PB][3];
+#pragma unroll
+                        for (int b = 0; b < PB; ++b) {
+                            const uint4* row = ix.codes + (size_t)rid[b] * W;
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                const uint32_t w = sub + (c0 + c) * g_;
+                                buf[b][c] = (rid[b] != kSentinel && c0 + c < cpl && w < W)
+                                                ? ldg_chunk(row + w)
+                                                : qv[c];
+                            }
+                        }
+#pragma unroll
+                        for (int b = 0; b < PB; ++b)
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) acc[b] += sm2_chunk(qv[c], buf[b][c]);
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < PB; ++b) {
+                    if (CPL) {
+#pragma unroll
+                        for (int off = G >> 1; off > 0; off >>= 1)
+                            acc[b] += __shfl_xor_sync(kFull, acc[b], off);
+                    } else {
+                        for (uint32_t off = g_ >> 1; off > 0; off >>= 1)
+                            acc[b] += __shfl_xor_sync(kFull, acc[b], off);
+                    }
+                    // contender test on the row's leader lane; row order is
+                    // (b0, b, grp), i.e. lane order within a pass
+                    const uint64_t key = mkkey(acc[b], rid[b]);
+                    bool c = sub == 0 && rid[b] != kSentinel && key < worst;
+                    uint32_t rp = 0;
+                    if (c) {
+                        rp = lower_bound_key(pk, np, key);
+                        if (rp < np && ordk(pk[rp]) == key) {
+                            c = false;  // already pooled (visited-table miss)
+                            ++c_drop;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(kFull, c);
+                    if (c) {
+                        const uint32_t pos = m + __popc(bal & lt_mask);
+                        ctd[pos] = key;
+                        crp[pos] = rp;
+                    }
+                    m += __popc(bal);
+                }
+            }
+            __syncwarp();
+
+            if (m > 0) {
+                // (b) contender ranks (key order) and prefix counts (row order)
+                uint64_t y[RW];
+                uint32_t rk[RW], pre[RW], rp[RW];
+#pragma unroll
+                for (int i = 0; i < RW; ++i) {
+                    const uint32_t idx = lane + 32u * i;
+                    y[i] = idx < m ? ctd[idx] : kInfKey;
+                    rp[i] = idx < m ? crp[idx] : 0u;
+                    rk[i] = 0;
+                    pre[i] = 0;
+                }
+                for (uint32_t j = 0; j < m; ++j) {
+                    const uint64_t yj = ctd[j];
+#pragma unroll
+                    for (int i = 0; i < RW; ++i) {
+                        const uint32_t lt = yj < y[i];
+                        rk[i] += lt;
+                        pre[i] += lt & (j < lane + 32u * i);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < RW; ++i)
+                    if (lane + 32u * i < m) csrp[rk[i]] = rp[i];
+                __syncwarp();
+
+                // (c) in-place merge: P entries at index >= lo shift right by
+                // #{contenders with rank-in-P <= index}; walk chunks backwards so
+                // no entry is overwritten before it is read
+                const uint32_t lo = csrp[0];
+                const uint32_t total = np + m;
+                if (lo < np) {
+                    for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
+                        const uint32_t idx = (uint32_t)cb + lane;
+                        const bool mv = idx < np && idx >= lo;
+                        uint64_t p = 0;
+                        uint32_t npos = 0;
+                        if (mv) {
+                            p = pk[idx];
+                            npos = idx + upper_bound_u32(csrp, m, idx);
+                        }
+                        __syncwarp();
+                        if (mv) {
+                            if (npos < ef) pk[npos] = p;
+                            else evk[npos - ef] = p;  // exp bit set = not a tie candidate
+                        }
+                        __syncwarp();
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < RW; ++i) {
+                    if (lane + 32u * i < m) {
+                        const uint32_t npos = rk[i] + rp[i];
+                        if (npos < ef) pk[npos] = y[i];
+                        else evk[npos - ef] = (rp[i] + pre[i]) < ef ? y[i] : (y[i] | kExp);
+                    }
+                }
+                __syncwarp();
+                if (lo < hint) hint = lo;
+
+                // (d) tie stack maintenance
+                if (total > ef) {
+                    const uint32_t wd = kdist(pk[ef - 1]);
+                    if (tn == 0 || wd < tdist) {
+                        tn = 0;
+                        tdist = wd;
+                    }
+                    const uint32_t nev = total - ef;
+                    uint32_t adds = 0;
+                    for (uint32_t e0 = 0; e0 < nev; e0 += 32) {
+                        const uint32_t e = e0 + lane;
+                        uint32_t idv = kSentinel;
+                        if (e < nev) {
+                            const uint64_t kk = evk[e];
+                            if (!(kk & kExp) && kdist(kk) == wd) idv = (uint32_t)kk;
+                        }
+                        const unsigned b = __ballot_sync(kFull, idv != kSentinel);
+                        if (idv != kSentinel) stg[adds + __popc(b & lt_mask)] = idv;
+                        adds += __popc(b);
+                    }
+                    if (adds) {
+                        __syncwarp();
+                        const uint32_t room = a.tie_cap - tn;
+                        if (adds > room) overflow = true;
+                        const uint32_t put = adds < room ? adds : room;
+                        // smallest key on top of the stack
+                        for (uint32_t r = lane; r < put; r += 32) tie[tn + put - 1 - r] = stg[r];
+                        tn += put;
+                        if (tn > c_maxtie) c_maxtie = tn;
+                    }
+                }
+                np = total < ef ? total : ef;
+                __syncwarp();
+            }
+
+            // (e) pick: first unexpanded pool entry at or after the hint, else
+            // the top of the tie stack (every live tie entry has dist ==
+            // worst(P).dist, so the reference's stop test, search.cpp:48, does
+            // not fire for it)
+            uint32_t u = kSentinel;
+            for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
+                const uint32_t idx = b0 + lane;
+                const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
                 const unsigned bal = __ballot_sync(kFull, un);
                 if (bal) {
-                    pick = 32 * e + __ffs(bal) - 1;
+                    const uint32_t pick = b0 + __ffs(bal) - 1;
+                    u = (uint32_t)pk[pick];
+                    __syncwarp();
+                    if (lane == 0) pk[pick] |= kExp;
+                    hint = pick + 1;
                     break;
                 }
             }
-            uint32_t u;
-            if (pick >= 0) {
-                u = (uint32_t)pk[pick];
-                __syncwarp();
-                if (lane == 0) pf[pick] = 1;
-            } else if (tn > 0) {
-                // every live tie entry has dist == worst(P).dist: the reference's
-                // stop test (search.cpp:48, dist-only, strict) does not fire
+            if (u == kSentinel) {
+                hint = np;
+                if (tn == 0) break;
                 u = tie[tn - 1];
                 --tn;
                 ++c_tie;
-            } else {
-                break;
             }
             ++c_exp;
 
-            // 2. adjacency row (stored order), vectorised, sentinel = unused slot
+            // (f) adjacency row (stored order), vectorised, sentinel = unused slot
             uint32_t v[RW];
             {
                 const uint32_t* row = ix.adj + (size_t)u * ix.RS;
@@ -305,29 +460,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                     } else if (RW == 2) {
                         const uint2 t = __ldg(reinterpret_cast<const uint2*>(row) + lane);
                         v[0] = t.x;
-                        v[1] = t.y;
+                        v[RW - 1] = t.y;
                     } else {
                         const uint4 t = __ldg(reinterpret_cast<const uint4*>(row) + lane);
                         v[0] = t.x;
-                        v[1] = t.y;
-                        if (RW > 2) {
-                            v[2 % RW] = t.z;
-                            v[3 % RW] = t.w;
-                        }
+                        v[1 % RW] = t.y;
+                        v[2 % RW] = t.z;
+                        v[3 % RW] = t.w;
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < RW; ++j) v[j] = kSentinel;
                 }
             }
-            // 3. visited filter (slot s = lane*RW + j; rows carry no duplicates)
+            // (g) visited filter + compaction (slot s = lane*RW + j; rows carry
+            // no duplicate ids, see adj_relayout_kernel)
             bool keep[RW];
-            unsigned deg_bal = 0;
 #pragma unroll
             for (int j = 0; j < RW; ++j) {
                 const uint32_t id = v[j];
                 bool k2 = id != kSentinel;
-                deg_bal += __popc(__ballot_sync(kFull, k2));
                 if (k2) {
                     if (xbits) {
                         const uint32_t bit = 1u << (id & 31);
@@ -340,178 +492,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                 }
                 keep[j] = k2;
             }
-            c_slots += deg_bal;
-            uint32_t n = 0, pos = 0;
+            uint32_t pos = 0, slots = 0;
+            n = 0;
 #pragma unroll
             for (int j = 0; j < RW; ++j) {
                 const unsigned b = __ballot_sync(kFull, keep[j]);
+                slots += __popc(__ballot_sync(kFull, v[j] != kSentinel));
                 pos += __popc(b & lt_mask);
                 n += __popc(b);
             }
+            c_slots += slots;
+            __syncwarp();  // previous readers of cid are done
 #pragma unroll
             for (int j = 0; j < RW; ++j)
                 if (keep[j]) cid[pos++] = v[j];
             __syncwarp();
-            if (n == 0) continue;
-            c_eval += n;
-
-            // 4. gather codes + SM2 distances -> cand[r] (row order)
-            gather(n);
-            __syncwarp();
-
-            // 5. contenders: c < max(P) (or P not full), not already in P
-            const uint64_t worst = np == ef ? pk[ef - 1] : kInfKey;
-            uint64_t x[RW];
-            bool isc[RW];
-#pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const uint32_t r = lane + 32u * i;
-                x[i] = r < n ? cand[r] : kInfKey;
-                bool c2 = x[i] < worst;
-                if (c2) {
-                    const uint32_t rp = lower_bound_u64(pk, np, x[i]);
-                    if (rp < np && pk[rp] == x[i]) {
-                        c2 = false;
-                        ++c_drop;  // per-lane count, reduced at the end
-                    }
-                }
-                isc[i] = c2;
-            }
-            uint32_t m = 0;
-            pos = 0;
-#pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const unsigned b = __ballot_sync(kFull, isc[i]);
-                // row order r = lane + 32 i  ->  order by (i, lane)
-                const uint32_t before = m + __popc(b & lt_mask);
-                if (isc[i]) ctd[before] = x[i];
-                m += __popc(b);
-            }
-            __syncwarp();
-            if (m == 0) continue;
-
-            // 6. contender ranks (among contenders) and prefix counts (row order)
-            uint64_t y[RW];
-            uint32_t rk[RW], pre[RW], rp[RW];
-#pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const uint32_t idx = lane + 32u * i;
-                y[i] = idx < m ? ctd[idx] : kInfKey;
-                rk[i] = 0;
-                pre[i] = 0;
-            }
-            for (uint32_t j = 0; j < m; ++j) {
-                const uint64_t yj = ctd[j];
-#pragma unroll
-                for (int i = 0; i < RW; ++i) {
-                    const uint32_t lt = yj < y[i];
-                    rk[i] += lt;
-                    pre[i] += lt & (j < lane + 32u * i);
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const uint32_t idx = lane + 32u * i;
-                rp[i] = idx < m ? lower_bound_u64(pk, np, y[i]) : 0u;
-                if (idx < m) cs[rk[i]] = y[i];  // sorted contenders
-            }
-            __syncwarp();
-
-            // 7. merge into the other pool buffer; evicted keys -> evk/evf
-            const uint32_t total = np + m;
-            const uint32_t newnp = total < ef ? total : ef;
-            uint64_t wkey = 0;
-            bool haveW = false;
-            for (uint32_t idx = lane; idx < np; idx += 32) {
-                const uint64_t p = pk[idx];
-                const uint8_t f = pf[idx];
-                const uint32_t npos = idx + lower_bound_u64(cs, m, p);
-                if (npos < ef) {
-                    pk2[npos] = p;
-                    pf2[npos] = f;
-                } else {
-                    evk[npos - ef] = p;
-                    evf[npos - ef] = f == 0;  // unexpanded -> tie candidate
-                }
-                if (npos == ef - 1) {
-                    wkey = p;
-                    haveW = true;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < RW; ++i) {
-                const uint32_t idx = lane + 32u * i;
-                if (idx < m) {
-                    const uint32_t npos = rk[i] + rp[i];
-                    if (npos < ef) {
-                        pk2[npos] = y[i];
-                        pf2[npos] = 0;
-                    } else {
-                        evk[npos - ef] = y[i];
-                        evf[npos - ef] = (rp[i] + pre[i]) < ef;  // admitted, then evicted
-                    }
-                    if (npos == ef - 1) {
-                        wkey = y[i];
-                        haveW = true;
-                    }
-                }
-            }
-            {
-                const unsigned hb = __ballot_sync(kFull, haveW);
-                if (hb) wkey = __shfl_sync(kFull, wkey, __ffs(hb) - 1);
-            }
-            __syncwarp();
-
-            // 8. tie stack maintenance
-            if (total > ef) {
-                const uint32_t wd = (uint32_t)(wkey >> 32);
-                if (tn == 0 || wd < tdist) {
-                    tn = 0;
-                    tdist = wd;
-                }
-                const uint32_t nev = total - ef;
-                uint32_t* stg = reinterpret_cast<uint32_t*>(base + L.stg);
-                uint32_t adds = 0;
-                for (uint32_t b0 = 0; b0 < nev; b0 += 32) {
-                    const uint32_t e = b0 + lane;
-                    uint32_t idv = kSentinel;
-                    if (e < nev) {
-                        const uint64_t kk = evk[e];
-                        if (evf[e] && (uint32_t)(kk >> 32) == wd) idv = (uint32_t)kk;
-                    }
-                    const unsigned b = __ballot_sync(kFull, idv != kSentinel);
-                    if (idv != kSentinel) stg[adds + __popc(b & lt_mask)] = idv;
-                    adds += __popc(b);
-                }
-                __syncwarp();
-                const uint32_t room = a.tie_cap - tn;
-                if (adds > room) overflow = true;
-                const uint32_t put = adds < room ? adds : room;
-                // smallest key on top of the stack
-                for (uint32_t r = lane; r < put; r += 32) tie[tn + put - 1 - r] = stg[r];
-                tn += put;
-                if (tn > c_maxtie) c_maxtie = tn;
-                __syncwarp();
-            }
-            // swap pool buffers
-            {
-                uint64_t* t1 = pk;
-                pk = pk2;
-                pk2 = t1;
-                uint8_t* t2 = pf;
-                pf = pf2;
-                pf2 = t2;
-            }
-            np = newnp;
         }
 
         // ---- outputs ------------------------------------------------------------
-        // reduce per-lane in-pool drop counts
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
         if (a.pool_ids) {
             for (uint32_t i = lane; i < ef; i += 32) {
                 a.pool_ids[q * ef + i] = i < np ? (uint32_t)pk[i] : kSentinel;
-                a.pool_dists[q * ef + i] = i < np ? (uint32_t)(pk[i] >> 32) : kSentinel;
+                a.pool_dists[q * ef + i] = i < np ? kdist(pk[i]) : kSentinel;
             }
             if (lane == 0) a.pool_n[q] = np;
         }
@@ -578,50 +581,39 @@ __global__ void pair_distance_kernel(const DevIndex ix, const uint4* __restrict_
     out[t] = d;
 }
 
-template <int EFW, int RW>
-using KernelPtr = void (*)(const SearchLaunch, const uint32_t, const uint32_t);
-
-constexpr int kPB = 4;
-
-template <int RW>
-void* pick_kernel_ef(uint32_t efw) {
-    switch (efw) {
-        case 1: return (void*)search_kernel<1, RW, kPB>;
-        case 2: return (void*)search_kernel<2, RW, kPB>;
-        case 4: return (void*)search_kernel<4, RW, kPB>;
-        case 8: return (void*)search_kernel<8, RW, kPB>;
-        case 16: return (void*)search_kernel<16, RW, kPB>;
-        default: return (void*)search_kernel<32, RW, kPB>;
-    }
-}
-
-void* pick_kernel(uint32_t efw, uint32_t rw) {
-    if (rw == 1) return pick_kernel_ef<1>(efw);
-    if (rw == 2) return pick_kernel_ef<2>(efw);
-    return pick_kernel_ef<4>(efw);
-}
-
 uint32_t pow2ceil(uint32_t x) {
     uint32_t p = 1;
     while (p < x) p <<= 1;
     return p;
 }
 
+template <int RW>
+void* pick_kernel_geom(uint32_t W, uint32_t* G) {
+    switch (W) {
+        case 6: *G = 2; return (void*)search_kernel<RW, 2, 3, 2>;
+        case 12: *G = 4; return (void*)search_kernel<RW, 4, 3, 4>;
+        case 24: *G = 8; return (void*)search_kernel<RW, 8, 3, 4>;
+        case 48: *G = 16; return (void*)search_kernel<RW, 16, 3, 4>;
+        default: {
+            uint32_t g = pow2ceil((W + 2) / 3);
+            *G = g > 32 ? 32 : g;
+            return (void*)search_kernel<RW, 1, 0, 4>;
+        }
+    }
+}
+
 struct Plan {
     void* fn;
-    uint32_t efw, rw, G, warp_bytes, block_bytes;
+    uint32_t rw, G, warp_bytes, block_bytes;
 };
 
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap) {
     Plan p;
-    p.efw = pow2ceil((ef + 31) / 32);
     p.rw = pow2ceil((ix.R + 31) / 32);
-    p.G = pow2ceil((ix.W + 2) / 3);
-    if (p.G > 32) p.G = 32;
-    p.fn = pick_kernel(p.efw, p.rw);
-    // the tie-add staging area lives in the cid region beyond RM/4 words: needs
-    // RM u32 more -> cid region is 4*RM bytes; staging uses [RM/4, RM/4 + RM)
-    const SmemLayout L = smem_layout(p.efw * 32, p.rw * 32, ix.W, tie_cap, 1u << vis_log2);
+    if (p.rw == 1) p.fn = pick_kernel_geom<1>(ix.W, &p.G);
+    else if (p.rw == 2) p.fn = pick_kernel_geom<2>(ix.W, &p.G);
+    else p.fn = pick_kernel_geom<4>(ix.W, &p.G);
+    const SmemLayout L = smem_layout((ef + 31) & ~31u, p.rw * 32, ix.W, tie_cap, 1u << vis_log2);
     p.warp_bytes = L.total;
     p.block_bytes = p.warp_bytes * kWarpsPerBlock;
     return p;
