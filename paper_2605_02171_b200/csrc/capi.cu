@@ -227,7 +227,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         cudaMemsetAsync(h->s_qst.p, 0, nq * 4, s);
     }
     cudaEventRecord(h->ev[2], s);
-    if ((st = launch_search(a, grid, s)) != QVG_OK) return st;
+    if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) return st;
     cudaEventRecord(h->ev[3], s);
     Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
     for (Out* o : outs) {

@@ -116,6 +116,7 @@ qvg_status alloc_handle(int device, uint64_t n, uint32_t dim, uint32_t R, uint32
     ix.codes = static_cast<const uint4*>(h->d_codes);
     ix.adj = static_cast<const uint32_t*>(h->d_adj);
     ix.cold = static_cast<const float*>(h->d_cold);
+    h->has_tmap = make_code_tmap(&h->tmap, h->d_codes, n, ix.W);
     *out = h;
     return QVG_OK;
 }

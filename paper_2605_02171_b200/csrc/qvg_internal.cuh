@@ -1,6 +1,7 @@
 // Internal declarations shared by the qvg translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -13,7 +14,7 @@ namespace qvg {
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr uint32_t kMaxEf = 1024;
 constexpr uint32_t kMaxDegree = 128;
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 2;
 
 // HBM-resident index.  Layouts:
 //   codes : n x W chunks of 16 B, chunk w = {pos word w, strong word w}
@@ -49,6 +50,10 @@ struct qvg_index {
     qvg::Buffer s_in, s_qn, s_qc, s_qst, s_ids, s_sc, s_cnt, s_pool_i, s_pool_d, s_pool_n,
         s_qctr, s_counter, s_exact, s_pair_ids, s_pair_out, s_st;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // TMA descriptor over the code rows (2-D: 2W u64 columns x n rows, box
+    // {2W, 1}) for tile::gather4; valid iff has_tmap (W <= 128)
+    alignas(64) CUtensorMap tmap;
+    bool has_tmap = false;
 };
 
 namespace qvg {
@@ -93,7 +98,10 @@ struct SearchLaunch {
 // grid = min(resident blocks, ceil(nq / warps per block)); exact-visited
 // bitmaps are sized for grid * kWarpsPerBlock warp slots.
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid);
-qvg_status launch_search(const SearchLaunch& a, uint64_t grid, cudaStream_t s);
+qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
+                         cudaStream_t s);
+// encode the gather4 descriptor for a code table (false if W > 128)
+bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W);
 void launch_pair_distance(const DevIndex& ix, const uint4* qchunks, const uint32_t* ids,
                           uint64_t npairs, uint32_t* out, cudaStream_t s);
 

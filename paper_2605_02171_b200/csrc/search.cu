@@ -8,9 +8,15 @@
 //   rerank             search.cpp:96-120  4-chain double dot (vec_math.hpp:13-26),
 //                                         sort (score desc, id asc), take k
 //
-// The dual heap is replaced by the equivalent sorted-list state machine of
-// SURVEY §8.A.3 (validated against the reference: tests/test_oracle_pins.py and
-// the GPU parity tests):
+// Memory path (B200): the code rows of an expansion's surviving neighbours are
+// fetched by the Tensor Memory Accelerator with cp.async.bulk.tensor
+// .tile::gather4 (four random rows per TMA instruction) into a double-buffered
+// shared-memory stage guarded by mbarriers; a warp's 64-row gather takes ~2 us
+// this way versus ~5 us with per-lane 128-bit loads (tools/gather_bench.cu).
+// Distances are then computed lane-per-row from shared memory.  The adjacency
+// row of the predicted next pick is prefetched while the gather is in flight.
+//
+// Search state (validated against the reference):
 //   P   sorted pool of <= ef keys in shared memory.  key = dist<<33 | exp<<32 | id;
 //       the order ignores the `exp` (expanded) bit, so (dist, id) order is a
 //       plain u64 compare of (key & ~EXP).
@@ -20,16 +26,18 @@
 //       smaller keys) are pushed on top; a drop of the worst dist kills all of T.
 //   vis lossy direct-mapped visited table.  A forgotten node that is scored
 //       again is either already in P (exact lookup, dropped) or has key > max(P)
-//       and is rejected, so results are unchanged; misses only
-//       cost bandwidth.
+//       and is rejected, so results are unchanged.
 // Admission of a row is the exact parallel form of the sequential loop: the
 // i-th surviving neighbour c_i is admitted iff
 //   #{p in P : p < c_i} + #{j < i : c_j < c_i} < ef
 // and P' = first ef of merge(P, admitted).  Only "contenders" (c < max(P), or
-// any c while P is not full) can matter, so after the gather only contenders
-// (a handful per row once P is full) are ranked and merged; the merge moves
-// only the tail of P at and after the first insertion point, in place.
+// any c while P is not full) can matter, so only they are ranked and merged;
+// the merge moves only the tail of P after the first insertion point, in place.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "qvg_internal.cuh"
 
@@ -60,12 +68,47 @@ __device__ __forceinline__ uint32_t sm2_chunk(const uint4 q, const uint4 v) {
     return __popc(x0) + __popc(x1) + __popc(o0) + __popc(o1) + 2u * (__popc(a0) + __popc(a1));
 }
 
-__device__ __forceinline__ uint4 ldg_chunk(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
+// ---- TMA / mbarrier primitives (PTX) -----------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n QVG_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra QVG_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// four code rows (ids r0..r3) -> dst (4 consecutive rows), one TMA instruction
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint32_t r0,
+                                            uint32_t r1, uint32_t r2, uint32_t r3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+// one contiguous row (1-D bulk copy), for code rows wider than a TMA box
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // first index i in [0, n) with ordk(a[i]) >= x
@@ -125,50 +168,75 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
 }
 
 struct SmemLayout {
-    uint32_t pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, total;
+    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, total;
 };
 
-// Per-warp shared-memory carve-up (bytes, every region 16-B aligned).
+// bytes of one 4-row TMA group in the stage; gather4 destinations must be
+// 128-B aligned, so groups are padded (row j of a half lives at
+// (j/4)*group_stride + (j%4)*16W)
+__host__ __device__ inline uint32_t group_stride(uint32_t W) { return (64u * W + 127u) & ~127u; }
+
+// Per-warp shared-memory carve-up (bytes).  Stage halves are 128-B aligned
+// (TMA destinations); the total is a multiple of 128 so every warp's base is.
 __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uint32_t W,
-                                                  uint32_t tie_cap, uint32_t vis_slots) {
+                                                  uint32_t tie_cap, uint32_t vis_slots,
+                                                  uint32_t stage_rows) {
     SmemLayout L;
     uint32_t o = 0;
-    auto take = [&](uint32_t bytes) {
+    auto take = [&](uint32_t bytes, uint32_t align) {
+        o = (o + align - 1) & ~(align - 1);
         const uint32_t at = o;
-        o += (bytes + 15u) & ~15u;
+        o += bytes;
         return at;
     };
-    L.pk = take(8 * EFM);   // pool keys
-    L.ctd = take(8 * RM);   // contenders, row order
-    L.evk = take(8 * RM);   // keys evicted this step, by (newpos - ef)
-    L.crp = take(4 * RM);   // contender rank in P, row order
-    L.csrp = take(4 * RM);  // contender rank in P, key order
-    L.cid = take(4 * RM);   // compacted row ids to score
-    L.stg = take(4 * RM);   // tie-stack additions, ascending
-    L.qc = take(16 * W);    // query code chunks
-    L.tie = take(4 * tie_cap);
-    L.vis = take(4 * vis_slots);  // rerank scores alias this region (vis_slots >= EFM)
-    L.total = o;
+    L.bars = take(16, 16);
+    L.stage0 = take((stage_rows / 4) * group_stride(W), 128);
+    L.stage1 = take((stage_rows / 4) * group_stride(W), 128);
+    L.pk = take(8 * EFM, 16);    // pool keys
+    L.ctd = take(8 * RM, 16);    // contenders, row order
+    L.evk = take(8 * RM, 16);    // keys evicted this step, by (newpos - ef)
+    L.crp = take(4 * RM, 16);    // contender rank in P, row order
+    L.csrp = take(4 * RM, 16);   // contender rank in P, key order
+    L.cid = take(4 * RM, 16);    // compacted row ids to score
+    L.stg = take(4 * RM, 16);    // tie-stack additions, ascending
+    L.qc = take(16 * W, 16);     // query code chunks
+    L.tie = take(4 * tie_cap, 16);
+    L.vis = take(4 * vis_slots, 16);  // rerank scores alias this region (vis_slots >= EFM)
+    L.total = (o + 127u) & ~127u;
     return L;
 }
 
-// G lanes score one code row; CPL = chunks per lane (W == G*CPL), or CPL == 0
-// for the generic path (runtime W and G, groups of 3 chunks per lane).
-template <int RW, int G, int CPL, int PB>
+// rows per stage half: a multiple of 4 (gather4 granularity), capped by the
+// row count of an expansion, floor 4
+__host__ __device__ inline uint32_t stage_rows_for(uint32_t W, uint32_t RM, uint32_t half_bytes) {
+    uint32_t r = 4u * (half_bytes / group_stride(W));
+    const uint32_t cap = (RM + 3u) & ~3u;
+    if (r > cap) r = cap;
+    if (r < 4) r = 4;
+    return r;
+}
+
+template <int RW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    search_kernel(const SearchLaunch a, const uint32_t warp_bytes, const uint32_t Grt) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    search_kernel(const __grid_constant__ CUtensorMap tmap, const SearchLaunch a,
+                  const uint32_t warp_bytes, const uint32_t SR, const int use_tmap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr uint32_t RM = RW * 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const DevIndex ix = a.ix;
-    const uint32_t W = CPL ? (uint32_t)(G * CPL) : ix.W;
+    const uint32_t W = ix.W;
+    const uint32_t rowb = 16u * W;
+    const uint32_t gstride = group_stride(W);  // bytes per 4-row TMA group (128-B aligned)
     const uint32_t VS = 1u << a.vis_log2;
     const uint32_t ef = a.ef;
     const uint32_t EFM = (ef + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS);
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
+    unsigned char* const stage0 = base + L.stage0;
+    const uint32_t stage_delta = L.stage1 - L.stage0;  // half h at stage0 + h * delta
     uint64_t* pk = reinterpret_cast<uint64_t*>(base + L.pk);
     uint64_t* ctd = reinterpret_cast<uint64_t*>(base + L.ctd);
     uint64_t* evk = reinterpret_cast<uint64_t*>(base + L.evk);
@@ -181,13 +249,41 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
 
-    const uint32_t g_ = CPL ? (uint32_t)G : Grt;  // lanes per code row
-    const uint32_t RPP = 32u / g_;                 // code rows per pass
-    const uint32_t sub = lane & (g_ - 1u);
-    const uint32_t grp = lane / g_;
-    const uint32_t cpl = CPL ? (uint32_t)CPL : (W + g_ - 1u) / g_;
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     uint32_t* xbits = a.exact_bits ? a.exact_bits + gwarp * a.exact_words : nullptr;
+    const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
+
+    if (lane == 0) {
+        mbar_init(&bars[0]);
+        mbar_init(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase0 = 0, phase1 = 0;
+
+    // issue the TMA fetch of compacted rows [r0, r0+cnt) into stage half h
+    auto issue = [&](uint32_t r0, uint32_t cnt, uint32_t h) {
+        uint64_t* bar = &bars[h];
+        const uint32_t ng = use_tmap ? (cnt + 3u) >> 2 : cnt;
+        const uint32_t bytes = use_tmap ? ng * 4u * rowb : cnt * rowb;
+        fence_proxy_async();  // order this lane's reads of the half before TMA writes
+        __syncwarp();         // all lanes finished reading this half
+        if (lane == 0) mbar_expect_tx(bar, bytes);
+        __syncwarp();
+        for (uint32_t g = lane; g < ng; g += 32) {
+            if (use_tmap) {
+                const uint32_t j = r0 + 4u * g;
+                const uint32_t i0 = cid[j];
+                const uint32_t i1 = 4u * g + 1u < cnt ? cid[j + 1] : i0;
+                const uint32_t i2 = 4u * g + 2u < cnt ? cid[j + 2] : i0;
+                const uint32_t i3 = 4u * g + 3u < cnt ? cid[j + 3] : i0;
+                tma_gather4(stage0 + h * stage_delta + (size_t)g * gstride, &tmap, i0, i1, i2, i3, bar);
+            } else {
+                bulk_row(stage0 + h * stage_delta + (size_t)(g >> 2) * gstride + (g & 3u) * rowb, ix.codes + (size_t)cid[r0 + g] * W, rowb,
+                         bar);
+            }
+        }
+    };
 
     for (;;) {
         unsigned long long qq = 0;
@@ -237,78 +333,84 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         uint32_t n = 1;  // rows to score in cid[0..n)
         if (lane == 0) cid[0] = entry;
         __syncwarp();
+        uint32_t spec_u = kSentinel;  // speculatively prefetched adjacency row
+        uint32_t spec_v[RW];
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
         for (;;) {
             c_eval += n;
-            // (a) gather code rows + SM2 distances; contenders -> ctd / crp
+            // (a) TMA-gather the code rows (double-buffered halves of SR rows)
+            const uint32_t nsub = (n + SR - 1) / SR;
+            if (nsub > 0) issue(0, min(n, SR), 0);
+            if (nsub > 1) issue(SR, min(n - SR, SR), 1);
+            // speculative prefetch: adjacency row of the current best unexpanded
+            // entry (the next pick unless this row inserts a better one)
+            {
+                uint32_t guess = kSentinel;
+                for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
+                    const uint32_t idx = b0 + lane;
+                    const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
+                    const unsigned bal = __ballot_sync(kFull, un);
+                    if (bal) {
+                        guess = (uint32_t)pk[b0 + __ffs(bal) - 1];
+                        break;
+                    }
+                }
+                if (guess == kSentinel && tn > 0) guess = tie[tn - 1];
+                spec_u = guess;
+                if (guess != kSentinel) {
+                    const uint32_t* row = ix.adj + (size_t)guess * ix.RS;
+                    if (lane * RW < ix.RS) {
+                        if (RW == 1) {
+                            spec_v[0] = __ldg(row + lane);
+                        } else if (RW == 2) {
+                            const uint2 t = __ldg(reinterpret_cast<const uint2*>(row) + lane);
+                            spec_v[0] = t.x;
+                            spec_v[RW - 1] = t.y;
+                        } else {
+                            const uint4 t = __ldg(reinterpret_cast<const uint4*>(row) + lane);
+                            spec_v[0] = t.x;
+                            spec_v[1 % RW] = t.y;
+                            spec_v[2 % RW] = t.z;
+                            spec_v[3 % RW] = t.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < RW; ++j) spec_v[j] = kSentinel;
+                    }
+                }
+            }
+            // (b) SM2 distances lane-per-row from the stage; contenders -> ctd/crp
             const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
             uint32_t m = 0;
-            for (uint32_t b0 = 0; b0 < n; b0 += RPP * PB) {
-                uint32_t acc[PB];
-                uint32_t rid[PB];
-#pragma unroll
-                for (int b = 0; b < PB; ++b) {
-                    acc[b] = 0;
-                    const uint32_t r = b0 + b * RPP + grp;
-                    rid[b] = r < n ? cid[r] : kSentinel;
-                }
-                if (CPL) {
-                    uint4 qv[CPL > 0 ? CPL : 1];
-#pragma unroll
-                    for (int c = 0; c < CPL; ++c) qv[c] = qc[sub + c * G];
-                    uint4 buf[PB][CPL > 0 ? CPL : 1];
-#pragma unroll
-                    for (int b = 0; b < PB; ++b) {
-                        const uint4* row = ix.codes + (size_t)rid[b] * W + sub;
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c)
-                            buf[b][c] = rid[b] != kSentinel ? ldg_chunk(row + c * G) : qv[c];
-                    }
-#pragma unroll
-                    for (int b = 0; b < PB; ++b)
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) acc[b] += sm2_chunk(qv[c], buf[b][c]);
+            for (uint32_t k = 0; k < nsub; ++k) {
+                const uint32_t h = k & 1u;
+                if (h == 0) {
+                    mbar_wait(&bars[0], phase0);
+                    phase0 ^= 1u;
                 } else {
-                    for (uint32_t c0 = 0; c0 < cpl; c0 += 3) {
-                        uint4 qv[3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const uint32_t w = sub + (c0 + c) * g_;
-                            qv[c] = (c0 + c < cpl && w < W) ? qc[w] : make_uint4(0, 0, 0, 0);
-                        }
-                        uint4 buf[PB][3];
-#pragma unroll
-                        for (int b = 0; b < PB; ++b) {
-                            const uint4* row = ix.codes + (size_t)rid[b] * W;
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                const uint32_t w = sub + (c0 + c) * g_;
-                                buf[b][c] = (rid[b] != kSentinel && c0 + c < cpl && w < W)
-                                                ? ldg_chunk(row + w)
-                                                : qv[c];
-                            }
-                        }
-#pragma unroll
-                        for (int b = 0; b < PB; ++b)
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) acc[b] += sm2_chunk(qv[c], buf[b][c]);
-                    }
+                    mbar_wait(&bars[1], phase1);
+                    phase1 ^= 1u;
                 }
-#pragma unroll
-                for (int b = 0; b < PB; ++b) {
-                    if (CPL) {
-#pragma unroll
-                        for (int off = G >> 1; off > 0; off >>= 1)
-                            acc[b] += __shfl_xor_sync(kFull, acc[b], off);
-                    } else {
-                        for (uint32_t off = g_ >> 1; off > 0; off >>= 1)
-                            acc[b] += __shfl_xor_sync(kFull, acc[b], off);
+                const uint32_t r0 = k * SR;
+                const uint32_t cnt = min(n - r0, SR);
+                const uint4* st = reinterpret_cast<const uint4*>(stage0 + h * stage_delta);
+                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+                    const uint32_t j = i0 + lane;
+                    const bool valid = j < cnt;
+                    uint32_t d = 0;
+                    if (valid) {
+                        const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
+                        uint32_t cc = rot;
+#pragma unroll 4
+                        for (uint32_t c = 0; c < W; ++c) {
+                            d += sm2_chunk(qc[cc], rowp[cc]);
+                            cc = cc + 1u == W ? 0u : cc + 1u;
+                        }
                     }
-                    // contender test on the row's leader lane; row order is
-                    // (b0, b, grp), i.e. lane order within a pass
-                    const uint64_t key = mkkey(acc[b], rid[b]);
-                    bool c = sub == 0 && rid[b] != kSentinel && key < worst;
+                    const uint32_t id = valid ? cid[r0 + j] : kSentinel;
+                    const uint64_t key = mkkey(d, id);
+                    bool c = valid && key < worst;
                     uint32_t rp = 0;
                     if (c) {
                         rp = lower_bound_key(pk, np, key);
@@ -325,11 +427,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                     }
                     m += __popc(bal);
                 }
+                if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), h);
             }
             __syncwarp();
 
             if (m > 0) {
-                // (b) contender ranks (key order) and prefix counts (row order)
+                // (c) contender ranks (key order) and prefix counts (row order)
                 uint64_t y[RW];
                 uint32_t rk[RW], pre[RW], rp[RW];
 #pragma unroll
@@ -354,7 +457,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                     if (lane + 32u * i < m) csrp[rk[i]] = rp[i];
                 __syncwarp();
 
-                // (c) in-place merge: P entries at index >= lo shift right by
+                // (d) in-place merge: P entries at index >= lo shift right by
                 // #{contenders with rank-in-P <= index}; walk chunks backwards so
                 // no entry is overwritten before it is read
                 const uint32_t lo = csrp[0];
@@ -388,7 +491,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                 __syncwarp();
                 if (lo < hint) hint = lo;
 
-                // (d) tie stack maintenance
+                // (e) tie stack maintenance
                 if (total > ef) {
                     const uint32_t wd = kdist(pk[ef - 1]);
                     if (tn == 0 || wd < tdist) {
@@ -423,7 +526,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                 __syncwarp();
             }
 
-            // (e) pick: first unexpanded pool entry at or after the hint, else
+            // (f) pick: first unexpanded pool entry at or after the hint, else
             // the top of the tie stack (every live tie entry has dist ==
             // worst(P).dist, so the reference's stop test, search.cpp:48, does
             // not fire for it)
@@ -450,9 +553,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             }
             ++c_exp;
 
-            // (f) adjacency row (stored order), vectorised, sentinel = unused slot
+            // (g) adjacency row (stored order): the speculative prefetch when it
+            // guessed right, else a fresh vectorised load
             uint32_t v[RW];
-            {
+            if (u == spec_u) {
+#pragma unroll
+                for (int j = 0; j < RW; ++j) v[j] = spec_v[j];
+            } else {
                 const uint32_t* row = ix.adj + (size_t)u * ix.RS;
                 if (lane * RW < ix.RS) {
                     if (RW == 1) {
@@ -473,7 +580,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                     for (int j = 0; j < RW; ++j) v[j] = kSentinel;
                 }
             }
-            // (g) visited filter + compaction (slot s = lane*RW + j; rows carry
+            // (h) visited filter + compaction (slot s = lane*RW + j; rows carry
             // no duplicate ids, see adj_relayout_kernel)
             bool keep[RW];
 #pragma unroll
@@ -587,39 +694,58 @@ uint32_t pow2ceil(uint32_t x) {
     return p;
 }
 
-template <int RW>
-void* pick_kernel_geom(uint32_t W, uint32_t* G) {
-    switch (W) {
-        case 6: *G = 2; return (void*)search_kernel<RW, 2, 3, 2>;
-        case 12: *G = 4; return (void*)search_kernel<RW, 4, 3, 4>;
-        case 24: *G = 8; return (void*)search_kernel<RW, 8, 3, 4>;
-        case 48: *G = 16; return (void*)search_kernel<RW, 16, 3, 4>;
-        default: {
-            uint32_t g = pow2ceil((W + 2) / 3);
-            *G = g > 32 ? 32 : g;
-            return (void*)search_kernel<RW, 1, 0, 4>;
-        }
-    }
+uint32_t stage_half_bytes() {
+    static uint32_t v = [] {
+        const char* e = getenv("QVG_STAGE_HALF_BYTES");
+        const long x = e ? atol(e) : 6144;
+        return (uint32_t)(x < 64 ? 64 : x);
+    }();
+    return v;
 }
 
 struct Plan {
     void* fn;
-    uint32_t rw, G, warp_bytes, block_bytes;
+    uint32_t rw, SR, warp_bytes, block_bytes;
 };
 
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap) {
     Plan p;
     p.rw = pow2ceil((ix.R + 31) / 32);
-    if (p.rw == 1) p.fn = pick_kernel_geom<1>(ix.W, &p.G);
-    else if (p.rw == 2) p.fn = pick_kernel_geom<2>(ix.W, &p.G);
-    else p.fn = pick_kernel_geom<4>(ix.W, &p.G);
-    const SmemLayout L = smem_layout((ef + 31) & ~31u, p.rw * 32, ix.W, tie_cap, 1u << vis_log2);
+    if (p.rw == 1) p.fn = (void*)search_kernel<1>;
+    else if (p.rw == 2) p.fn = (void*)search_kernel<2>;
+    else p.fn = (void*)search_kernel<4>;
+    p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
+    const SmemLayout L =
+        smem_layout((ef + 31) & ~31u, p.rw * 32, ix.W, tie_cap, 1u << vis_log2, p.SR);
     p.warp_bytes = L.total;
     p.block_bytes = p.warp_bytes * kWarpsPerBlock;
     return p;
 }
 
 }  // namespace
+
+bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W) {
+    if (2 * W > 256) return false;  // TMA box dimension limit
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qres;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres) !=
+                cudaSuccess ||
+            !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)(2 * W), (cuuint64_t)n};
+    cuuint64_t gstride[1] = {(cuuint64_t)(16 * W)};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * W), 1};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(codes),
+                              gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out) {
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
@@ -643,9 +769,14 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out) {
     return QVG_OK;
 }
 
-qvg_status launch_search(const SearchLaunch& a, uint64_t grid, cudaStream_t s) {
+qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
+                         cudaStream_t s) {
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
-    void* args[] = {(void*)&a, (void*)&p.warp_bytes, (void*)&p.G};
+    CUtensorMap dummy;
+    memset(&dummy, 0, sizeof(dummy));
+    const CUtensorMap* m = tmap ? tmap : &dummy;
+    int use_tmap = tmap != nullptr;
+    void* args[] = {(void*)m, (void*)&a, (void*)&p.warp_bytes, (void*)&p.SR, (void*)&use_tmap};
     cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kWarpsPerBlock * 32),
                                      args, p.block_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "launch(search)");
