@@ -91,6 +91,10 @@ typedef struct qvg_stats {
     double search_ms;          /* device time of the fused search+rerank kernel */
     double device_ms;          /* encode + search (device, excl. copies) */
     double total_ms;           /* incl. host<->device copies when host buffers */
+    uint32_t grid_blocks;      /* persistent grid of the search kernel */
+    uint32_t warps_per_block;
+    uint32_t smem_per_block;   /* dynamic shared memory bytes */
+    uint32_t resident_warps_per_sm;
 } qvg_stats;
 
 /* Search options for qvg_search_ex. */

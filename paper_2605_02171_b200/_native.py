@@ -37,7 +37,9 @@ class qvg_stats(C.Structure):
         "queries", "expansions", "tie_expansions", "dist_evals", "inpool_drops",
         "adjacency_slots", "cold_accesses", "tie_overflows", "max_tie_depth",
         "adjacency_bytes", "code_bytes", "rerank_bytes", "io_bytes")] + [
-        (n, C.c_double) for n in ("encode_ms", "search_ms", "device_ms", "total_ms")]
+        (n, C.c_double) for n in ("encode_ms", "search_ms", "device_ms", "total_ms")] + [
+        (n, C.c_uint32) for n in ("grid_blocks", "warps_per_block", "smem_per_block",
+                                  "resident_warps_per_sm")]
 
     def to_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

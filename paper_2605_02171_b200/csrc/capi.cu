@@ -197,7 +197,15 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     a.qctr = static_cast<uint32_t*>(o_ctr.dev);
     a.counter = static_cast<unsigned long long*>(h->s_counter.p);
     uint64_t grid = 0;
-    if ((st = plan_search(a, h->device, &grid)) != QVG_OK) return st;
+    {
+        static const uint32_t variant = [] {
+            const char* v = getenv("QVG_VARIANT");
+            return v ? (uint32_t)strtoul(v, nullptr, 0) : 0u;
+        }();
+        a.variant = variant;
+    }
+    PlanInfo pinfo;
+    if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;
     if (exact) {
         const uint64_t words = ((ix.n + 31) / 32 + 3) & ~3ull;
         if ((st = grow(h->s_exact, grid * kWarpsPerBlock * words * 4)) != QVG_OK) return st;
@@ -263,6 +271,10 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         stats->device_ms = t;
         cudaEventElapsedTime(&t, h->ev[0], h->ev[4]);
         stats->total_ms = t;
+        stats->grid_blocks = (uint32_t)grid;
+        stats->warps_per_block = pinfo.warps_per_block;
+        stats->smem_per_block = pinfo.smem_per_block;
+        stats->resident_warps_per_sm = pinfo.resident_warps_per_sm;
         stats->queries = nq;
         if (counters) {
             const uint32_t* c = o_ctr.copy_back ? out_qctr : ctr_host.data();

@@ -91,13 +91,19 @@ struct SearchLaunch {
     uint32_t* qctr;
     unsigned long long* counter;
     uint32_t* flags;        // atomicOr(1 << QVG_Q_TIE_OVERFLOW) on overflow
+    uint32_t variant;       // A/B switches (QVG_VARIANT env): bit0 no rerank L2 prefetch,
+                            // bit1 paired-half distance pass
     uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
     uint64_t exact_words;   // words per slot
 };
 
 // grid = min(resident blocks, ceil(nq / warps per block)); exact-visited
 // bitmaps are sized for grid * kWarpsPerBlock warp slots.
-qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid);
+struct PlanInfo {
+    uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0;
+};
+qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid,
+                       PlanInfo* info = nullptr);
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s);
 // encode the gather4 descriptor for a code table (false if W > 128)

@@ -98,6 +98,16 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
         : "memory");
 }
+// four rows x one box of columns starting at column `col` (cold-store slices)
+__device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* map, uint32_t col,
+                                                uint32_t r0, uint32_t r1, uint32_t r2,
+                                                uint32_t r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
 // one contiguous row (1-D bulk copy), for code rows wider than a TMA box
 __device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
@@ -106,6 +116,10 @@ __device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// warm L2 with a contiguous range (TMA bulk prefetch; size multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -133,8 +147,17 @@ __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t 
     return lo;
 }
 
+__device__ __forceinline__ float4 ldg_f4_noalloc(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
 // 4 strided double chains combined as (s0+s1)+(s2+s3) (vec_math.hpp:13-26).
 // Products of floats are exact in double, so FMA == mul+add here.
+template <bool NOALLOC>
 __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
                                             const float* __restrict__ v, uint32_t dim) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -142,10 +165,10 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
     const float4* v4 = reinterpret_cast<const float4*>(v);
     const uint32_t n4 = dim >> 2;
     uint32_t t = 0;
-    for (; t + 8 <= n4; t += 8) {
+    for (; t + 8 <= n4; t += 8) {  // 128 B of the row in flight per lane
         float4 b[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) b[u] = __ldg(v4 + t + u);
+        for (int u = 0; u < 8; ++u) b[u] = NOALLOC ? ldg_f4_noalloc(v4 + t + u) : __ldg(v4 + t + u);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const float4 a = __ldg(q4 + t + u);
@@ -168,7 +191,7 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
 }
 
 struct SmemLayout {
-    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, total;
+    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, qsl, total;
 };
 
 // bytes of one 4-row TMA group in the stage; gather4 destinations must be
@@ -194,14 +217,15 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.stage1 = take((stage_rows / 4) * group_stride(W), 128);
     L.pk = take(8 * EFM, 16);    // pool keys
     L.ctd = take(8 * RM, 16);    // contenders, row order
-    L.evk = take(8 * RM, 16);    // keys evicted this step, by (newpos - ef)
+    L.evk = L.ctd;               // keys evicted this step (ctd is dead by then)
     L.crp = take(4 * RM, 16);    // contender rank in P, row order
     L.csrp = take(4 * RM, 16);   // contender rank in P, key order
     L.cid = take(4 * RM, 16);    // compacted row ids to score
-    L.stg = take(4 * RM, 16);    // tie-stack additions, ascending
+    L.stg = L.crp;               // tie-stack additions (crp is dead by then)
     L.qc = take(16 * W, 16);     // query code chunks
     L.tie = take(4 * tie_cap, 16);
     L.vis = take(4 * vis_slots, 16);  // rerank scores alias this region (vis_slots >= EFM)
+    L.qsl = take(2 * 48 * 4, 16);     // rerank query slices (one per stage half)
     L.total = (o + 127u) & ~127u;
     return L;
 }
@@ -218,8 +242,9 @@ __host__ __device__ inline uint32_t stage_rows_for(uint32_t W, uint32_t RM, uint
 
 template <int RW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    search_kernel(const __grid_constant__ CUtensorMap tmap, const SearchLaunch a,
-                  const uint32_t warp_bytes, const uint32_t SR, const int use_tmap) {
+    search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
+                  const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
+                  const int use_tmap, const uint32_t SL) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr uint32_t RM = RW * 32;
     const uint32_t lane = threadIdx.x & 31;
@@ -248,6 +273,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     uint32_t* tie = reinterpret_cast<uint32_t*>(base + L.tie);
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
+    float* qsl = reinterpret_cast<float*>(base + L.qsl);
 
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     uint32_t* xbits = a.exact_bits ? a.exact_bits + gwarp * a.exact_words : nullptr;
@@ -314,6 +340,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         }
 
         // ---- per-query init --------------------------------------------------
+        const long long t_start = clock64();  // phase timers (variant bit 4: debug)
         for (uint32_t w = lane; w < W; w += 32) qc[w] = a.qcodes[q * W + w];
         if (xbits) {
             uint4* xb4 = reinterpret_cast<uint4*>(xbits);
@@ -383,7 +410,76 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             // (b) SM2 distances lane-per-row from the stage; contenders -> ctd/crp
             const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
             uint32_t m = 0;
-            for (uint32_t k = 0; k < nsub; ++k) {
+            // contender test + row-order compaction of one scored row per lane
+            auto emit = [&](bool valid, uint32_t d, uint32_t id) {
+                const uint64_t key = mkkey(d, id);
+                bool c = valid && key < worst;
+                uint32_t rp = 0;
+                if (c) {
+                    rp = lower_bound_key(pk, np, key);
+                    if (rp < np && ordk(pk[rp]) == key) {
+                        c = false;  // already pooled (visited-table miss)
+                        ++c_drop;
+                    }
+                }
+                const unsigned bal = __ballot_sync(kFull, c);
+                if (c) {
+                    const uint32_t pos = m + __popc(bal & lt_mask);
+                    ctd[pos] = key;
+                    crp[pos] = rp;
+                }
+                m += __popc(bal);
+            };
+            // paired pass (wait for both halves, then score 2 rows per lane) is
+            // opt-in: measured slower than overlapping half-0 scoring with the
+            // arrival of half 1 (tools/tune_search.py, cfg2: 3.95 vs 3.03 ms)
+            const bool paired = SR <= 32 && (a.variant & 2u);
+            if (paired) {
+                // both halves in flight at once; each lane scores row j of each
+                // half in one pass over the chunks (shared query loads, 2x ILP).
+                // Chunks are visited from a per-lane rotation (bank spreading) as
+                // two straight ranges [rot, W) and [0, rot).
+                for (uint32_t k = 0; k < nsub; k += 2) {
+                    mbar_wait(&bars[0], phase0);
+                    phase0 ^= 1u;
+                    const bool two = k + 1 < nsub;
+                    if (two) {
+                        mbar_wait(&bars[1], phase1);
+                        phase1 ^= 1u;
+                    }
+                    const uint32_t cnt0 = min(n - k * SR, SR);
+                    const uint32_t cnt1 = two ? min(n - (k + 1) * SR, SR) : 0u;
+                    const bool v0 = lane < cnt0, v1 = lane < cnt1;
+                    const uint32_t roff = ((lane >> 2) * gstride + (lane & 3u) * rowb) / 16u;
+                    const uint4* r0p = reinterpret_cast<const uint4*>(stage0) + roff;
+                    const uint4* r1p = reinterpret_cast<const uint4*>(stage0 + stage_delta) + roff;
+                    uint32_t d0 = 0, d1 = 0;
+                    if (v0 && v1) {
+#pragma unroll 4
+                        for (uint32_t p = rot; p < W; ++p) {
+                            const uint4 qv = qc[p];
+                            d0 += sm2_chunk(qv, r0p[p]);
+                            d1 += sm2_chunk(qv, r1p[p]);
+                        }
+#pragma unroll 4
+                        for (uint32_t p = 0; p < rot; ++p) {
+                            const uint4 qv = qc[p];
+                            d0 += sm2_chunk(qv, r0p[p]);
+                            d1 += sm2_chunk(qv, r1p[p]);
+                        }
+                    } else if (v0) {
+#pragma unroll 4
+                        for (uint32_t p = rot; p < W; ++p) d0 += sm2_chunk(qc[p], r0p[p]);
+#pragma unroll 4
+                        for (uint32_t p = 0; p < rot; ++p) d0 += sm2_chunk(qc[p], r0p[p]);
+                    }
+                    emit(v0, d0, v0 ? cid[k * SR + lane] : kSentinel);
+                    if (two) emit(v1, d1, v1 ? cid[(k + 1) * SR + lane] : kSentinel);
+                    if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), 0);
+                    if (k + 3 < nsub) issue((k + 3) * SR, min(n - (k + 3) * SR, SR), 1);
+                }
+            }
+            for (uint32_t k = 0; !paired && k < nsub; ++k) {
                 const uint32_t h = k & 1u;
                 if (h == 0) {
                     mbar_wait(&bars[0], phase0);
@@ -408,24 +504,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                             cc = cc + 1u == W ? 0u : cc + 1u;
                         }
                     }
-                    const uint32_t id = valid ? cid[r0 + j] : kSentinel;
-                    const uint64_t key = mkkey(d, id);
-                    bool c = valid && key < worst;
-                    uint32_t rp = 0;
-                    if (c) {
-                        rp = lower_bound_key(pk, np, key);
-                        if (rp < np && ordk(pk[rp]) == key) {
-                            c = false;  // already pooled (visited-table miss)
-                            ++c_drop;
-                        }
-                    }
-                    const unsigned bal = __ballot_sync(kFull, c);
-                    if (c) {
-                        const uint32_t pos = m + __popc(bal & lt_mask);
-                        ctd[pos] = key;
-                        crp[pos] = rp;
-                    }
-                    m += __popc(bal);
+                    emit(valid, d, valid ? cid[r0 + j] : kSentinel);
                 }
                 if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), h);
             }
@@ -617,6 +696,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         }
 
         // ---- outputs ------------------------------------------------------------
+        const long long t_search = clock64();
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
         if (a.pool_ids) {
             for (uint32_t i = lane; i < ef; i += 32) {
@@ -645,11 +725,105 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             // rerank: one lane per pool entry, 4 sequential double chains
             const float* qv = a.qn + q * ix.Dp;
             __syncwarp();
-            for (uint32_t idx = lane; idx < np; idx += 32) {
-                const uint32_t id = (uint32_t)pk[idx];
-                sc[idx] = dot4_exact(qv, ix.cold + (size_t)id * ix.Dp, ix.dim);
+            if (SL) {
+                // TMA column slices: round t stages slice (t % nsl) of the 32 pool
+                // rows of group (t / nsl) — 4 rows x SL floats per gather4 —
+                // into a stage half; lane r owns row 32g + r and advances its 4
+                // chains slice by slice, i.e. in ascending element order, which
+                // keeps every chain's rounding sequence identical to dot_f32.
+                const uint32_t dim = ix.dim;
+                const uint32_t main4 = dim & ~3u;
+                const uint32_t nsl = (dim + SL - 1) / SL;
+                const uint32_t rounds = ((np + 31) / 32) * nsl;
+                const uint32_t cgs = (16u * SL + 127u) & ~127u;  // bytes per 4-row group
+                auto rr_issue = [&](uint32_t t) {
+                    const uint32_t g = t / nsl, s = t % nsl, h = t & 1u;
+                    const uint32_t rows = min(32u, np - 32u * g);
+                    const uint32_t ng4 = (rows + 3u) >> 2;
+                    // the query slice rides in the same transaction (16-B multiple,
+                    // clipped to the padded row so the last query never overreads)
+                    const uint32_t qbytes = 4u * min(SL, ix.Dp - s * SL);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_expect_tx(&bars[h], ng4 * 16u * SL + qbytes);
+                        bulk_row(qsl + h * 48u, qv + s * SL, qbytes, &bars[h]);
+                    }
+                    __syncwarp();
+                    if (lane < ng4) {
+                        const uint32_t j = 32u * g + 4u * lane;
+                        const uint32_t i0 = (uint32_t)pk[j];
+                        const uint32_t i1 = 4u * lane + 1u < rows ? (uint32_t)pk[j + 1] : i0;
+                        const uint32_t i2 = 4u * lane + 2u < rows ? (uint32_t)pk[j + 2] : i0;
+                        const uint32_t i3 = 4u * lane + 3u < rows ? (uint32_t)pk[j + 3] : i0;
+                        tma_gather4_col(stage0 + h * stage_delta + lane * cgs, &cmap, s * SL, i0, i1,
+                                        i2, i3, &bars[h]);
+                    }
+                };
+                if (rounds > 0) rr_issue(0);
+                if (rounds > 1) rr_issue(1);
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                for (uint32_t t = 0; t < rounds; ++t) {
+                    const uint32_t g = t / nsl, s = t % nsl, h = t & 1u;
+                    // the round's query slice -> registers in one batch of
+                    // independent loads, issued before the stage wait (qn is
+                    // L2-resident; L1 is mostly carved out for shared memory)
+                    constexpr uint32_t kMaxSL4 = 12;  // rerank_slice() caps SL at 48
+                    const uint32_t i0 = s * SL;
+                    const uint32_t lim = min(SL, dim - i0);
+                    const float4* qr = reinterpret_cast<const float4*>(qsl) + h * (kMaxSL4);
+                    if (h == 0) {
+                        mbar_wait(&bars[0], phase0);
+                        phase0 ^= 1u;
+                    } else {
+                        mbar_wait(&bars[1], phase1);
+                        phase1 ^= 1u;
+                    }
+                    if (s == 0) s0 = s1 = s2 = s3 = 0.0;
+                    const uint32_t row = 32u * g + lane;
+                    if (row < np) {
+                        const float4* rp = reinterpret_cast<const float4*>(
+                            stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
+#pragma unroll
+                        for (uint32_t u = 0; u < kMaxSL4; ++u) {
+                            if (4u * u >= lim) break;
+                            const uint32_t i = i0 + 4u * u;
+                            const float4 v = rp[u];
+                            const float4 qq = qr[u];
+                            if (i + 4 <= main4) {
+                                s0 = __fma_rn((double)qq.x, (double)v.x, s0);
+                                s1 = __fma_rn((double)qq.y, (double)v.y, s1);
+                                s2 = __fma_rn((double)qq.z, (double)v.z, s2);
+                                s3 = __fma_rn((double)qq.w, (double)v.w, s3);
+                            } else {  // tail elements >= 4*floor(D/4) all go to s0
+                                if (i < dim) s0 = __fma_rn((double)qq.x, (double)v.x, s0);
+                                if (i + 1 < dim) s0 = __fma_rn((double)qq.y, (double)v.y, s0);
+                                if (i + 2 < dim) s0 = __fma_rn((double)qq.z, (double)v.z, s0);
+                            }
+                        }
+                        if (s == nsl - 1)
+                            sc[row] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                    }
+                    if (t + 2 < rounds) rr_issue(t + 2);
+                }
+            } else {
+                // fallback: one lane per pool entry streaming its row from global
+                if (!(a.variant & 1u))
+                    for (uint32_t idx = lane; idx < np; idx += 32)
+                        prefetch_l2(ix.cold + (size_t)(uint32_t)pk[idx] * ix.Dp, ix.Dp * 4u);
+                for (uint32_t idx = lane; idx < np; idx += 32) {
+                    const uint32_t id = (uint32_t)pk[idx];
+                    const float* row = ix.cold + (size_t)id * ix.Dp;
+                    sc[idx] = (a.variant & 4u) ? dot4_exact<true>(qv, row, ix.dim)
+                                               : dot4_exact<false>(qv, row, ix.dim);
+                }
             }
             __syncwarp();
+            const long long t_dots = clock64();
+            if ((a.variant & 16u) && lane == 0 && a.qctr) {
+                a.qctr[q * 8 + 0] = (uint32_t)((t_search - t_start) >> 4);
+                a.qctr[q * 8 + 1] = (uint32_t)((t_dots - t_search) >> 4);
+            }
             // rank by (score desc, id asc) and emit the first k
             for (uint32_t idx = lane; idx < np; idx += 32) {
                 const float si = sc[idx];
@@ -670,6 +844,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                 a.out_scores[q * a.k + r] = __int_as_float(0x7fc00000);
             }
             if (lane == 0 && a.out_count) a.out_count[q] = np < a.k ? np : a.k;
+            if ((a.variant & 16u) && lane == 0 && a.qctr)
+                a.qctr[q * 8 + 2] = (uint32_t)((clock64() - t_dots) >> 4);
         }
         __syncwarp();
     }
@@ -724,8 +900,9 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
 
 }  // namespace
 
-bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W) {
-    if (2 * W > 256) return false;  // TMA box dimension limit
+// 2-D row-gather descriptor: `cols` elements per row, `n` rows, box {box_cols, 1}
+static bool encode_rows_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t esize,
+                            const void* base, uint64_t cols, uint64_t n, uint32_t box_cols) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -736,18 +913,31 @@ bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W)
             return false;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    cuuint64_t gdim[2] = {(cuuint64_t)(2 * W), (cuuint64_t)n};
-    cuuint64_t gstride[1] = {(cuuint64_t)(16 * W)};
-    cuuint32_t box[2] = {(cuuint32_t)(2 * W), 1};
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)n};
+    cuuint64_t gstride[1] = {(cuuint64_t)(cols * esize)};
+    cuuint32_t box[2] = {box_cols, 1};
     cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(codes),
-                              gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = encode(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out) {
+bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W) {
+    if (2 * W > 256) return false;  // TMA box dimension limit
+    return encode_rows_map(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 8, codes, 2 * W, n, 2 * W);
+}
+
+// cold-store slice width (floats) for the rerank: 8 four-row groups of a
+// stage half, each 128-B aligned; 0 = no TMA rerank
+static uint32_t rerank_slice(uint32_t half_bytes) {
+    uint32_t sl = (half_bytes / 8u) / 16u;  // floats per row slice
+    sl &= ~7u;                                // 16*sl multiple of 128
+    if (sl > 48) sl = 48;                     // query slice held in 12 float4 registers
+    return sl >= 8 ? sl : 0u;
+}
+
+qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, PlanInfo* info) {
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
     cudaError_t e = cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)p.block_bytes);
@@ -766,17 +956,34 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out) {
     if (want < grid) grid = want;
     if (grid < 1) grid = 1;
     *grid_out = grid;
+    if (info) {
+        info->warps_per_block = kWarpsPerBlock;
+        info->smem_per_block = p.block_bytes;
+        info->resident_warps_per_sm = (uint32_t)per_sm * kWarpsPerBlock;
+    }
     return QVG_OK;
 }
 
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s) {
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
-    CUtensorMap dummy;
+    alignas(64) CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
     const CUtensorMap* m = tmap ? tmap : &dummy;
     int use_tmap = tmap != nullptr;
-    void* args[] = {(void*)m, (void*)&a, (void*)&p.warp_bytes, (void*)&p.SR, (void*)&use_tmap};
+    // cold-store slice map (per launch: the slice width follows the stage size)
+    alignas(64) CUtensorMap cmap;
+    uint32_t SL = 0;
+    if (a.do_rerank && !(a.variant & 8u)) {
+        const uint32_t half = (p.SR / 4u) * group_stride(a.ix.W);
+        SL = rerank_slice(half);
+        if (SL && !encode_rows_map(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.ix.cold, a.ix.Dp,
+                                   a.ix.n, SL))
+            SL = 0;
+    }
+    if (!SL) memset(&cmap, 0, sizeof(cmap));
+    void* args[] = {(void*)m,     (void*)&cmap,     (void*)&a, (void*)&p.warp_bytes,
+                    (void*)&p.SR, (void*)&use_tmap, (void*)&SL};
     cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kWarpsPerBlock * 32),
                                      args, p.block_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "launch(search)");

@@ -1,59 +1,100 @@
-"""Sweep search-kernel knobs (stage half bytes via env, visited slots) on a
-config; prints kernel ms / QPS.  Run on the GPU box:  python tools/tune_search.py 2"""
+"""A/B sweep of search-kernel knobs on a cached config graph (GPU box).
+
+    python tools/tune_search.py --config 2 --ef 64 \
+        --grid "QVG_STAGE_HALF_BYTES=6144,QVG_VARIANT=0;QVG_VARIANT=1" --vis 512,1024
+
+Each env setting runs in a fresh process (the library reads env at first use).
+Per setting: 3 warm-up launches, then 20 launches each preceded by a 256 MB L2
+flush; kernel time = the library's CUDA-event search_ms.  Prints min / median
+and the resident warps per SM, and checks ids against an exact-visited pass.
+"""
+import argparse
 import ctypes as C
+import json
 import os
 import subprocess
 import sys
-import json
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-if len(sys.argv) > 2 and sys.argv[2] == "child":
+
+def child(a):
     import numpy as np
     import torch
+
     import paper_2605_02171_b200 as Q
     from paper_2605_02171_b200 import _native as N, datasets, graphs
-    cfg = datasets.CONFIGS[int(sys.argv[1])]
-    base, queries = datasets.config_data(cfg, nq=10000)
-    g = graphs.load_graph(cfg, "literal", base.shape[0], base)
+    cfg = datasets.CONFIGS[a.config]
+    base, queries = datasets.config_data(cfg, nq=a.nq, sigma_mode=a.sigma_mode)
+    g = graphs.load_graph(cfg, a.sigma_mode, base.shape[0], base)
     qn, codes, _ = Q.encode_queries(base)
     ix = Q.GpuIndex.from_arrays(codes, g["adj"], qn, int(g["entry"]))
     del qn, codes
-    ef = int(sys.argv[4]) if len(sys.argv) > 4 else 64
-    ref = ix.search_ex(queries, k=10, ef=ef, exact_visited=True, pools=False)["ids"]
+    nq = len(queries)
+    ref = ix.search_ex(queries, k=10, ef=a.ef, exact_visited=True, pools=False)
     q = torch.from_numpy(queries).cuda()
-    ids = torch.empty((len(queries), 10), dtype=torch.int32, device="cuda")
-    sc = torch.empty((len(queries), 10), dtype=torch.float32, device="cuda")
-    cnt = torch.empty(len(queries), dtype=torch.int32, device="cuda")
-    stt = torch.empty(len(queries), dtype=torch.int32, device="cuda")
+    ids = torch.empty((nq, 10), dtype=torch.int32, device="cuda")
+    sc = torch.empty((nq, 10), dtype=torch.float32, device="cuda")
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    stt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     ix.set_stream(torch.cuda.current_stream())
     out = []
-    for vs in [int(x) for x in sys.argv[3].split(",")]:
-        opts = N.qvg_search_opts(visited_slots=vs, entry_point=N.SENTINEL, timing_only=1)
-        ks = []
-        for it in range(13):
+    for vs in [int(x) for x in a.vis.split(",")]:
+        opts = N.qvg_search_opts(visited_slots=vs, entry_point=N.SENTINEL, timing_only=1,
+                                 no_rerank=int(a.no_rerank))
+        ks, st = [], None
+        for it in range(23):
+            flush.zero_()
             st = N.qvg_stats()
-            rc = N.lib().qvg_search_ex(ix._h, q.data_ptr(), len(queries), 10, ef, C.byref(opts),
+            rc = N.lib().qvg_search_ex(ix._h, q.data_ptr(), nq, 10, a.ef, C.byref(opts),
                                        ids.data_ptr(), sc.data_ptr(), cnt.data_ptr(),
                                        stt.data_ptr(), None, None, None, None, C.byref(st))
             assert rc == 0, N.last_error()
             if it >= 3:
                 ks.append(st.search_ms)
-        same = bool((ids.cpu().numpy().view(np.uint32) == ref).all())
-        out.append(dict(vs=vs, ms=sorted(ks)[len(ks) // 2], same=same))
-    print(json.dumps(out))
-    sys.exit(0)
+        same = a.no_rerank or bool((ids.cpu().numpy().view(np.uint32) == ref["ids"]).all())
+        ks.sort()
+        out.append(dict(vis=vs, min=ks[0], med=ks[len(ks) // 2], same=same,
+                        warps=st.resident_warps_per_sm, smem=st.smem_per_block,
+                        grid=st.grid_blocks))
+    print("RESULT " + json.dumps(out))
 
-cfgn = sys.argv[1] if len(sys.argv) > 1 else "2"
-ef = sys.argv[2] if len(sys.argv) > 2 else "64"
-for stage in [3072, 6144, 12288]:
-    env = dict(os.environ, QVG_STAGE_HALF_BYTES=str(stage))
-    r = subprocess.run([sys.executable, __file__, cfgn, "child", "256,512,1024,2048", ef],
-                       env=env, capture_output=True, text=True)
-    if r.returncode:
-        print(stage, "FAILED", r.stderr[-2000:])
-        continue
-    for e in json.loads(r.stdout.strip().splitlines()[-1]):
-        print(f"stage_half={stage:6d} vis={e['vs']:5d} kernel={e['ms']:.3f} ms "
-              f"qps={10000 / e['ms'] * 1e3:,.0f} same={e['same']}")
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ef", type=int, default=64)
+    ap.add_argument("--nq", type=int, default=10000)
+    ap.add_argument("--sigma-mode", default="literal")
+    ap.add_argument("--vis", default="512,1024")
+    ap.add_argument("--grid", default="")
+    ap.add_argument("--child", action="store_true")
+    ap.add_argument("--no-rerank", action="store_true")
+    a = ap.parse_args()
+    if a.child:
+        child(a)
+        return
+    settings = [s for s in a.grid.split(";")] if a.grid else [""]
+    for s in settings:
+        env = dict(os.environ)
+        for kv in filter(None, s.split(",")):
+            k, v = kv.split("=")
+            env[k] = v
+        cmd = [sys.executable, __file__, "--child", "--config", str(a.config), "--ef", str(a.ef),
+               "--nq", str(a.nq), "--sigma-mode", a.sigma_mode, "--vis", a.vis] + (
+                   ["--no-rerank"] if a.no_rerank else [])
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+        lines = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")]
+        if r.returncode or not lines:
+            print(s or "(default)", "FAILED", r.stderr[-1500:])
+            continue
+        for e in json.loads(lines[-1][7:]):
+            print(f"{s or '(default)':45s} vis={e['vis']:5d} min={e['min']:.3f} "
+                  f"med={e['med']:.3f} ms qps(min)={a.nq / e['min'] * 1e3:,.0f} "
+                  f"warps/SM={e['warps']} smem/blk={e['smem']} same={e['same']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
