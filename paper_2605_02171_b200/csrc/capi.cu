@@ -143,14 +143,19 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         set_error("beam_search: invalid entry point");
         return QVG_INVALID_ARGUMENT;
     }
-    uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
-    if (!vslots) vslots = ef <= 64 ? 1024u : (ef <= 128 ? 2048u : 4096u);
-    if (vslots < 32 * ((ef + 31) / 32)) vslots = 32 * ((ef + 31) / 32);  // scores alias it
-    uint32_t vlog = log2_floor(vslots);
-    if ((1u << vlog) < vslots) ++vlog;
-    if (vlog < 5) vlog = 5;
     uint32_t tcap = opts && opts->tie_capacity ? opts->tie_capacity : (ef < 64 ? 64u : ef);
     tcap = (tcap + 3) & ~3u;
+    uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
+    uint32_t vlog;
+    if (vslots) {
+        if (vslots < 32 * ((ef + 31) / 32)) vslots = 32 * ((ef + 31) / 32);  // scores alias it
+        vlog = log2_floor(vslots);
+        if ((1u << vlog) < vslots) ++vlog;
+        if (vlog < 5) vlog = 5;
+    } else {
+        // largest table that keeps the most resident warps (occupancy-aware)
+        vlog = auto_visited_log2(ix, ef, tcap, h->device);
+    }
     const bool exact = opts && opts->exact_visited;
     const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
     const bool want_ctr = out_qctr != nullptr || (stats && !(opts && opts->timing_only));

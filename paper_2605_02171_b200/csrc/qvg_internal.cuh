@@ -99,6 +99,10 @@ struct SearchLaunch {
 
 // grid = min(resident blocks, ceil(nq / warps per block)); exact-visited
 // bitmaps are sized for grid * kWarpsPerBlock warp slots.
+// default visited-table size (log2 slots): the largest table (256..4096
+// slots, >= ef) among those that keep the maximum number of resident blocks
+uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device);
+
 struct PlanInfo {
     uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0;
 };

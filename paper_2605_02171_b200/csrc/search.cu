@@ -240,8 +240,16 @@ __host__ __device__ inline uint32_t stage_rows_for(uint32_t W, uint32_t RM, uint
     return r;
 }
 
+// register budget per template: enough blocks that shared memory, not
+// registers, bounds residency at the BASELINE geometries (R=32 rows -> ~9
+// blocks of 2 warps fit in smem; R=64 -> ~7)
 template <int RW>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+struct MinBlocks {
+    static constexpr int value = RW == 1 ? 9 : (RW == 2 ? 7 : 5);
+};
+
+template <int RW>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
                   const int use_tmap, const uint32_t SL) {
@@ -935,6 +943,33 @@ static uint32_t rerank_slice(uint32_t half_bytes) {
     sl &= ~7u;                                // 16*sl multiple of 128
     if (sl > 48) sl = 48;                     // query slice held in 12 float4 registers
     return sl >= 8 ? sl : 0u;
+}
+
+uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device) {
+    uint32_t min_log = 8;  // 256 slots
+    while ((1u << min_log) < ((ef + 31u) & ~31u)) ++min_log;
+    uint32_t best_log = min_log;
+    int best_blocks = -1;
+    for (uint32_t lg = min_log; lg <= 12 || lg == min_log; ++lg) {
+        const Plan p = make_plan(ix, ef, lg, tie_cap);
+        if (cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)p.block_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+        }
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, p.fn, kWarpsPerBlock * 32,
+                                                          p.block_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+        }
+        if (blocks >= best_blocks) {  // ties go to the larger table
+            best_blocks = blocks;
+            best_log = lg;
+        }
+    }
+    (void)device;
+    return best_log;
 }
 
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, PlanInfo* info) {

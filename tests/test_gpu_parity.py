@@ -271,6 +271,20 @@ def test_reference_reads_our_file_and_we_read_theirs(tmp_path):
     assert p2.read_bytes() == p.read_bytes()
 
 
+def test_cpp_dropin():
+    """include/qvg.hpp used exactly as a reference maintainer would: a
+    qivr::Index from qivr::build_index -> qvg::GpuIndex, and
+    qvg::run_query_batch == qivr::run_query_batch (ids + score bits), same
+    std::invalid_argument cases (tests/cpp/dropin_test.cpp)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(O.REF_SO), "qvg_dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in binary not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "dropin: OK" in p.stdout
+
+
 # ---------------------------------------------------------------- fresh graphs
 @ref_only
 @pytest.mark.parametrize("sigma_mode", ["literal", "norm"])

@@ -56,7 +56,9 @@ def child(a):
                 ks.append(st.search_ms)
         same = a.no_rerank or bool((ids.cpu().numpy().view(np.uint32) == ref["ids"]).all())
         ks.sort()
+        ev = ix.search_ex(queries, k=10, ef=a.ef, visited_slots=vs, pools=False)["stats"]
         out.append(dict(vis=vs, min=ks[0], med=ks[len(ks) // 2], same=same,
+                        evals=ev["dist_evals"] / nq, exact=ref["stats"]["dist_evals"] / nq,
                         warps=st.resident_warps_per_sm, smem=st.smem_per_block,
                         grid=st.grid_blocks))
     print("RESULT " + json.dumps(out))
@@ -93,7 +95,8 @@ def main():
         for e in json.loads(lines[-1][7:]):
             print(f"{s or '(default)':45s} vis={e['vis']:5d} min={e['min']:.3f} "
                   f"med={e['med']:.3f} ms qps(min)={a.nq / e['min'] * 1e3:,.0f} "
-                  f"warps/SM={e['warps']} smem/blk={e['smem']} same={e['same']}", flush=True)
+                  f"warps/SM={e['warps']} smem/blk={e['smem']} evals/q={e['evals']:.0f} "
+                  f"(exact {e['exact']:.0f}) same={e['same']}", flush=True)
 
 
 if __name__ == "__main__":
