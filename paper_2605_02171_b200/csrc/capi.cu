@@ -147,7 +147,10 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     tcap = (tcap + 3) & ~3u;
     uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
     uint32_t vlog;
-    if (vslots) {
+    auto cached = h->plans.find(qvg_index::PlanKey{ef, tcap, vslots});
+    if (cached != h->plans.end()) {
+        vlog = cached->second.first;
+    } else if (vslots) {
         if (vslots < 32 * ((ef + 31) / 32)) vslots = 32 * ((ef + 31) / 32);  // scores alias it
         vlog = log2_floor(vslots);
         if ((1u << vlog) < vslots) ++vlog;
@@ -209,8 +212,23 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         }();
         a.variant = variant;
     }
+    // launch plan, cached per (ef, tie capacity, visited request): occupancy
+    // queries cost host time that would otherwise leave the GPU idle per call
     PlanInfo pinfo;
-    if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;
+    {
+        const uint32_t vreq = opts && opts->visited_slots ? opts->visited_slots : 0u;
+        const qvg_index::PlanKey key{ef, tcap, vreq};
+        auto it = h->plans.find(key);
+        if (it == h->plans.end()) {
+            if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;
+            it = h->plans.emplace(key, std::make_pair(vlog, pinfo)).first;
+        }
+        pinfo = it->second.second;
+        const uint64_t want = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        const uint64_t full = (uint64_t)pinfo.resident_warps_per_sm / kWarpsPerBlock * pinfo.sms;
+        grid = want < full ? want : full;
+        if (grid < 1) grid = 1;
+    }
     if (exact) {
         const uint64_t words = ((ix.n + 31) / 32 + 3) & ~3ull;
         if ((st = grow(h->s_exact, grid * kWarpsPerBlock * words * 4)) != QVG_OK) return st;

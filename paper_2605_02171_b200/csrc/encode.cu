@@ -8,9 +8,14 @@
 //   encode_sm2_into        encoding.cpp:32-45  (pos = y > 0, strong = |y| > tau,
 //                          strict, pad bits zero)
 // The double reductions must run in index order to round identically, so one
-// thread owns one query; the batch supplies the parallelism (10k queries =
-// 10k threads).  All arithmetic uses explicit _rn intrinsics so no contraction
-// or fast-math can change a rounding.
+// lane owns one query; the batch supplies the parallelism.  A warp owns 32
+// consecutive queries and moves data through a transposed shared-memory tile,
+// so every global load/store instruction covers 128 contiguous bytes of one
+// row (a thread-per-row layout would touch 32 lines per instruction).  All
+// arithmetic uses explicit _rn intrinsics so no contraction can change a
+// rounding.
+#include <cstdlib>
+
 #include "qvg_internal.cuh"
 
 namespace qvg {
@@ -19,37 +24,41 @@ namespace {
 
 __device__ __forceinline__ bool finitef(float v) { return isfinite(v); }
 
-template <bool VEC4>
-__global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ x, uint64_t nq,
-                                                     uint32_t dim, uint32_t Dp,
-                                                     float* __restrict__ qn,
-                                                     uint4* __restrict__ qcodes,
-                                                     float* __restrict__ tau_out,
-                                                     int32_t* __restrict__ status,
-                                                     uint32_t* __restrict__ flags) {
-    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (q >= nq) return;
+__global__ void __launch_bounds__(128) encode_tiled_kernel(
+    const float* __restrict__ x, uint64_t nq, uint32_t dim, uint32_t Dp, float* __restrict__ qn,
+    uint4* __restrict__ qcodes, float* __restrict__ tau_out, int32_t* __restrict__ status,
+    uint32_t* __restrict__ flags) {
+    __shared__ float tile_all[4][32][33];  // +1 column: conflict-free transposes
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t q0 = ((uint64_t)blockIdx.x * 4 + wib) * 32;
+    if (q0 >= nq) return;
+    float(*T)[33] = tile_all[wib];
+    const uint64_t myq = q0 + lane;
+    const bool mine = myq < nq;
     const uint32_t W = (dim + 63) / 64;
-    const float* row = x + q * dim;
-    float* out = qn + q * Dp;
-    uint4* code = qcodes + q * W;
+    // columns [c0, c0+32) of the warp's 32 rows (row stride ld) -> T.  x goes
+    // through the read-only path; qn (written by this warp in pass 2) must use
+    // coherent loads.
+    auto load = [&](const float* src, uint64_t ld, uint32_t c0, bool readonly) {
+        __syncwarp();
+#pragma unroll 8
+        for (uint32_t r = 0; r < 32; ++r) {
+            const uint64_t q = q0 + r;
+            const float* p = src + q * ld + c0 + lane;
+            T[r][lane] = (q < nq && c0 + lane < dim) ? (readonly ? __ldg(p) : *p) : 0.0f;
+        }
+        __syncwarp();
+    };
 
-    // pass 1: finite check + sum of squares (vec_math.hpp:28-34)
+    // pass 1: finite check + sequential sum of squares (vec_math.hpp:28-34);
+    // x*x is exact in double, so the FMA rounds exactly like acc + x*x
     bool finite = true;
     double acc = 0.0;
-    if (VEC4) {
-        const float4* r4 = reinterpret_cast<const float4*>(row);
-        for (uint32_t i = 0; i < dim / 4; ++i) {
-            const float4 v = __ldg(r4 + i);
-            finite &= finitef(v.x) & finitef(v.y) & finitef(v.z) & finitef(v.w);
-            acc = __fma_rn((double)v.x, (double)v.x, acc);  // product exact in double
-            acc = __fma_rn((double)v.y, (double)v.y, acc);
-            acc = __fma_rn((double)v.z, (double)v.z, acc);
-            acc = __fma_rn((double)v.w, (double)v.w, acc);
-        }
-    } else {
-        for (uint32_t i = 0; i < dim; ++i) {
-            const float v = __ldg(row + i);
+    for (uint32_t c0 = 0; c0 < dim; c0 += 32) {
+        load(x, dim, c0, true);
+        const uint32_t lim = min(32u, dim - c0);
+        for (uint32_t j = 0; j < lim; ++j) {
+            const float v = T[lane][j];
             finite &= finitef(v);
             acc = __fma_rn((double)v, (double)v, acc);
         }
@@ -58,75 +67,143 @@ __global__ void __launch_bounds__(128) encode_kernel(const float* __restrict__ x
     if (!finite) st = QVG_Q_NONFINITE_COORD;
     const double norm = __dsqrt_rn(acc);
     if (st == QVG_Q_OK && (!(norm > 0.0) || isinf(norm))) st = QVG_Q_BAD_NORM;
-    if (st != QVG_Q_OK) {
-        status[q] = st;
-        if (flags) atomicOr(flags, 1u << st);
-        if (tau_out) tau_out[q] = 0.0f;
-        for (uint32_t i = 0; i < Dp; ++i) out[i] = 0.0f;
-        for (uint32_t w = 0; w < W; ++w) code[w] = make_uint4(0, 0, 0, 0);
-        return;
-    }
-    const float inv = __double2float_rn(__ddiv_rn(1.0, norm));
+    const float inv = st == QVG_Q_OK ? __double2float_rn(__ddiv_rn(1.0, norm)) : 0.0f;
 
-    // pass 2: y = x * inv (f32), finite check of y, sequential sum of |y|
+    // pass 2: y = x * inv (f32), finite check, sequential sum of |y|; store y
+    // (zero padding up to Dp)
     double s = 0.0;
     bool yfinite = true;
-    if (VEC4) {
-        const float4* r4 = reinterpret_cast<const float4*>(row);
-        float4* o4 = reinterpret_cast<float4*>(out);
-        for (uint32_t i = 0; i < dim / 4; ++i) {
-            const float4 v = __ldg(r4 + i);
-            float4 y;
-            y.x = __fmul_rn(v.x, inv);
-            y.y = __fmul_rn(v.y, inv);
-            y.z = __fmul_rn(v.z, inv);
-            y.w = __fmul_rn(v.w, inv);
-            yfinite &= finitef(y.x) & finitef(y.y) & finitef(y.z) & finitef(y.w);
-            s = __dadd_rn(s, fabs((double)y.x));
-            s = __dadd_rn(s, fabs((double)y.y));
-            s = __dadd_rn(s, fabs((double)y.z));
-            s = __dadd_rn(s, fabs((double)y.w));
-            o4[i] = y;
-        }
-    } else {
-        for (uint32_t i = 0; i < dim; ++i) {
-            const float y = __fmul_rn(__ldg(row + i), inv);
+    for (uint32_t c0 = 0; c0 < Dp; c0 += 32) {
+        load(x, dim, c0, true);
+        const uint32_t lim = c0 < dim ? min(32u, dim - c0) : 0u;
+        for (uint32_t j = 0; j < lim; ++j) {
+            const float y = st == QVG_Q_OK ? __fmul_rn(T[lane][j], inv) : 0.0f;
             yfinite &= finitef(y);
             s = __dadd_rn(s, fabs((double)y));
-            out[i] = y;
+            T[lane][j] = y;
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (uint32_t r = 0; r < 32; ++r) {
+            const uint64_t q = q0 + r;
+            if (q < nq && c0 + lane < Dp)
+                qn[q * Dp + c0 + lane] = c0 + lane < dim ? T[r][lane] : 0.0f;
         }
     }
-    for (uint32_t i = dim; i < Dp; ++i) out[i] = 0.0f;
-    if (!yfinite) {
-        status[q] = QVG_Q_NONFINITE_CODE;
-        if (flags) atomicOr(flags, 1u << QVG_Q_NONFINITE_CODE);
-        if (tau_out) tau_out[q] = 0.0f;
-        for (uint32_t w = 0; w < W; ++w) code[w] = make_uint4(0, 0, 0, 0);
-        return;
-    }
-    const float tau = __double2float_rn(__ddiv_rn(s, (double)dim));
+    if (st == QVG_Q_OK && !yfinite) st = QVG_Q_NONFINITE_CODE;
+    const float tau = st == QVG_Q_OK ? __double2float_rn(__ddiv_rn(s, (double)dim)) : 0.0f;
 
-    // pass 3: bit planes, little-endian within 64-bit words, pad bits zero
-    for (uint32_t w = 0; w < W; ++w) {
-        uint32_t p0 = 0, p1 = 0, s0 = 0, s1 = 0;
-        const uint32_t base = w * 64;
-        const uint32_t lim = min(64u, dim - base);
-        for (uint32_t b = 0; b < lim; ++b) {
-            const float y = out[base + b];
-            const uint32_t pbit = y > 0.0f;
-            const uint32_t sbit = fabsf(y) > tau;
-            if (b < 32) {
-                p0 |= pbit << b;
-                s0 |= sbit << b;
-            } else {
-                p1 |= pbit << (b - 32);
-                s1 |= sbit << (b - 32);
+    // pass 3: bit planes from y (re-read coalesced); a 32-column chunk is one
+    // half of a 64-bit word, little-endian; pad bits zero
+    uint32_t p_lo = 0, s_lo = 0;
+    for (uint32_t c0 = 0; c0 < W * 64; c0 += 32) {
+        uint32_t pb = 0, sb = 0;
+        if (c0 < dim) {
+            load(qn, Dp, c0, false);
+            const uint32_t lim = min(32u, dim - c0);
+            for (uint32_t j = 0; j < lim; ++j) {
+                const float y = T[lane][j];
+                pb |= (uint32_t)(y > 0.0f) << j;
+                sb |= (uint32_t)(fabsf(y) > tau) << j;
             }
         }
-        code[w] = make_uint4(p0, p1, s0, s1);
+        if (st != QVG_Q_OK) pb = sb = 0;
+        if ((c0 & 63) == 0) {
+            p_lo = pb;
+            s_lo = sb;
+        } else if (mine) {
+            qcodes[myq * W + c0 / 64] = make_uint4(p_lo, pb, s_lo, sb);
+        }
     }
-    status[q] = QVG_Q_OK;
-    if (tau_out) tau_out[q] = tau;
+    if (mine) {
+        status[myq] = st;
+        if (st != QVG_Q_OK && flags) atomicOr(flags, 1u << st);
+        if (tau_out) tau_out[myq] = tau;
+    }
+}
+
+// Warp-per-query variant: the row is loaded coalesced into shared memory, lane
+// 0 runs the two order-sensitive double reductions from shared memory (the
+// DFMA/DADD dependency chain is the cost, ~D steps), and all lanes do the
+// elementwise scaling, stores and bit packing.  With one warp per query the
+// batch provides thousands of warps to hide the chains' latency.
+__global__ void __launch_bounds__(256) encode_warp_kernel(
+    const float* __restrict__ x, uint64_t nq, uint32_t dim, uint32_t Dp, float* __restrict__ qn,
+    uint4* __restrict__ qcodes, float* __restrict__ tau_out, int32_t* __restrict__ status,
+    uint32_t* __restrict__ flags) {
+    extern __shared__ __align__(16) float rows_all[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t q = (uint64_t)blockIdx.x * 8 + wib;
+    if (q >= nq) return;
+    float* row = rows_all + (size_t)wib * Dp;
+    const float* src = x + q * dim;
+    const uint32_t W = (dim + 63) / 64;
+
+    bool finite = true;
+    for (uint32_t i = lane; i < dim; i += 32) {
+        const float v = __ldg(src + i);
+        finite &= finitef(v);
+        row[i] = v;
+    }
+    finite = __all_sync(0xFFFFFFFFu, finite);
+    __syncwarp();
+    // pass 1 (lane 0): sequential sum of squares (vec_math.hpp:28-34)
+    double inv_d = 0.0;
+    int32_t st = finite ? QVG_Q_OK : QVG_Q_NONFINITE_COORD;
+    if (lane == 0 && st == QVG_Q_OK) {
+        double acc = 0.0;
+#pragma unroll 8
+        for (uint32_t i = 0; i < dim; ++i) acc = __fma_rn((double)row[i], (double)row[i], acc);
+        const double norm = __dsqrt_rn(acc);
+        if (!(norm > 0.0) || isinf(norm)) st = QVG_Q_BAD_NORM;
+        else inv_d = __ddiv_rn(1.0, norm);
+    }
+    st = __shfl_sync(0xFFFFFFFFu, st, 0);
+    const float inv = __double2float_rn(__shfl_sync(0xFFFFFFFFu, inv_d, 0));
+    // y = x * inv, stored to smem and (coalesced) to qn with zero padding
+    bool yfinite = true;
+    for (uint32_t i = lane; i < Dp; i += 32) {
+        const float y = (i < dim && st == QVG_Q_OK) ? __fmul_rn(row[i], inv) : 0.0f;
+        yfinite &= finitef(y);
+        if (i < dim) row[i] = y;
+        qn[q * Dp + i] = y;
+    }
+    yfinite = __all_sync(0xFFFFFFFFu, yfinite);
+    if (st == QVG_Q_OK && !yfinite) st = QVG_Q_NONFINITE_CODE;
+    __syncwarp();
+    // pass 2 (lane 0): sequential sum of |y| -> tau (encoding.cpp:23-30)
+    float tau_l = 0.0f;
+    if (lane == 0 && st == QVG_Q_OK) {
+        double s = 0.0;
+#pragma unroll 8
+        for (uint32_t i = 0; i < dim; ++i) s = __dadd_rn(s, fabs((double)row[i]));
+        tau_l = __double2float_rn(__ddiv_rn(s, (double)dim));
+    }
+    const float tau = __shfl_sync(0xFFFFFFFFu, tau_l, 0);
+    // bit planes: lane w packs 64-bit word w
+    for (uint32_t w = lane; w < W; w += 32) {
+        uint32_t p0 = 0, p1 = 0, s0 = 0, s1 = 0;
+        if (st == QVG_Q_OK) {
+            const uint32_t b0 = w * 64, lim = min(64u, dim - b0);
+            for (uint32_t b = 0; b < lim; ++b) {
+                const float y = row[b0 + b];
+                const uint32_t pbit = y > 0.0f, sbit = fabsf(y) > tau;
+                if (b < 32) {
+                    p0 |= pbit << b;
+                    s0 |= sbit << b;
+                } else {
+                    p1 |= pbit << (b - 32);
+                    s1 |= sbit << (b - 32);
+                }
+            }
+        }
+        qcodes[q * W + w] = make_uint4(p0, p1, s0, s1);
+    }
+    if (lane == 0) {
+        status[q] = st;
+        if (st != QVG_Q_OK && flags) atomicOr(flags, 1u << st);
+        if (tau_out) tau_out[q] = tau;
+    }
 }
 
 // reference layout (W pos words, W strong words per row) -> 16-B chunks
@@ -158,12 +235,21 @@ void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float
                    uint4* qcodes, float* tau, int32_t* status, uint32_t* flags,
                    cudaStream_t s) {
     if (nq == 0) return;
-    const unsigned blocks = (unsigned)((nq + 127) / 128);
-    const bool vec4 = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    if (vec4)
-        encode_kernel<true><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
-    else
-        encode_kernel<false><<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
+    const size_t smem = 8ull * Dp * sizeof(float);
+    static int variant = [] {
+        const char* v = getenv("QVG_ENCODE");
+        return v ? atoi(v) : 0;
+    }();
+    if (variant == 1 || smem > 200 * 1024) {
+        const unsigned blocks = (unsigned)((nq + 127) / 128);
+        encode_tiled_kernel<<<blocks, 128, 0, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
+        return;
+    }
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(encode_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const unsigned blocks = (unsigned)((nq + 7) / 8);
+    encode_warp_kernel<<<blocks, 256, smem, s>>>(x, nq, dim, Dp, qn, qcodes, tau, status, flags);
 }
 
 void launch_codes_to_chunks(const uint64_t* ref_codes, uint64_t rows, uint32_t W, uint4* out,

@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
+#include <utility>
 
 #include "../../include/qvg.h"
 
@@ -34,6 +36,10 @@ struct Buffer {
     size_t bytes = 0;
 };
 
+struct PlanInfo {
+    uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0, sms = 0;
+};
+
 }  // namespace qvg
 
 struct qvg_index {
@@ -54,6 +60,14 @@ struct qvg_index {
     // {2W, 1}) for tile::gather4; valid iff has_tmap (W <= 128)
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
+    // launch plans keyed by (ef, tie capacity, visited-slot request)
+    struct PlanKey {
+        uint32_t ef, tcap, vreq;
+        bool operator<(const PlanKey& o) const {
+            return ef != o.ef ? ef < o.ef : (tcap != o.tcap ? tcap < o.tcap : vreq < o.vreq);
+        }
+    };
+    std::map<PlanKey, std::pair<uint32_t, qvg::PlanInfo>> plans;  // -> (vis_log2, info)
 };
 
 namespace qvg {
@@ -103,9 +117,6 @@ struct SearchLaunch {
 // slots, >= ef) among those that keep the maximum number of resident blocks
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device);
 
-struct PlanInfo {
-    uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0;
-};
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid,
                        PlanInfo* info = nullptr);
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,

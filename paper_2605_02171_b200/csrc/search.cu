@@ -945,6 +945,20 @@ static uint32_t rerank_slice(uint32_t half_bytes) {
     return sl >= 8 ? sl : 0u;
 }
 
+// opt-in dynamic shared memory per block on this device
+static uint32_t max_dyn_smem(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    return (uint32_t)v;
+}
+
+// Raise a kernel's dynamic-smem cap to the device maximum (monotone, so a
+// cached plan of any size stays launchable whatever was planned after it).
+static bool allow_max_smem(void* fn, int device) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)max_dyn_smem(device)) == cudaSuccess;
+}
+
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device) {
     uint32_t min_log = 8;  // 256 slots
     while ((1u << min_log) < ((ef + 31u) & ~31u)) ++min_log;
@@ -952,9 +966,7 @@ uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, in
     int best_blocks = -1;
     for (uint32_t lg = min_log; lg <= 12 || lg == min_log; ++lg) {
         const Plan p = make_plan(ix, ef, lg, tie_cap);
-        if (cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)p.block_bytes) != cudaSuccess) {
-            cudaGetLastError();
+        if (p.block_bytes > max_dyn_smem(device) || !allow_max_smem(p.fn, device)) {
             break;
         }
         int blocks = 0;
@@ -974,9 +986,12 @@ uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, in
 
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, PlanInfo* info) {
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
-    cudaError_t e = cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p.block_bytes);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(search)");
+    if (p.block_bytes > max_dyn_smem(device)) {
+        set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (!allow_max_smem(p.fn, device)) return cuda_status(cudaGetLastError(), "cudaFuncSetAttribute");
+    cudaError_t e;
     int per_sm = 0, sms = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.fn, kWarpsPerBlock * 32,
                                                       p.block_bytes);
@@ -995,6 +1010,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         info->warps_per_block = kWarpsPerBlock;
         info->smem_per_block = p.block_bytes;
         info->resident_warps_per_sm = (uint32_t)per_sm * kWarpsPerBlock;
+        info->sms = (uint32_t)sms;
     }
     return QVG_OK;
 }
