@@ -1,0 +1,100 @@
+"""GPU builder (qvg_build, secondary path ★(2)) vs the reference builder.
+Stage 0 must be exact (codes, normalised cold store, medoid entry point);
+stage 1 is batched, so the graph is judged statistically (degree stats,
+reachability, Recall@10 vs a reference-built graph on the same data)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")
+
+import paper_2605_02171_b200 as Q  # noqa: E402
+from paper_2605_02171_b200.datasets import mixture  # noqa: E402
+
+
+def reachable(adj, entry):
+    n = adj.shape[0]
+    seen = np.zeros(n, bool)
+    seen[entry] = True
+    stack = [entry]
+    while stack:
+        u = stack.pop()
+        for v in adj[u, 1:1 + adj[u, 0]]:
+            if not seen[v]:
+                seen[v] = True
+                stack.append(int(v))
+    return seen.mean()
+
+
+def build(data, m, ef_c, alpha=1.2, passes=1, batch=0, seed=42):
+    st = {}
+    ix = Q.GpuIndex.build(data, Q.BuildParams(m=m, ef_c=ef_c, alpha=alpha, passes=passes,
+                                              batch=batch, seed=seed), stats=st)
+    return ix, st
+
+
+@ref_only
+@pytest.mark.parametrize("passes", [1, 2])
+def test_build_stage0_exact_and_graph_quality(passes):
+    base, q = mixture(6000, 96, 40, 0.35, seed=5, nq=200, sigma_mode="norm")
+    ix, st = build(base, m=8, ef_c=48, passes=passes, batch=512)
+    codes, adj, cold = ix.export()
+    ref = O.RefIndex.build(base, m=8, ef_c=48, alpha=1.2, threads=4)
+    # stage 0 (builder.cpp:59-120) is exact
+    assert np.array_equal(codes, ref.codes())
+    assert np.array_equal(cold.view(np.uint32), ref.cold().view(np.uint32))
+    assert ix.entry_point == ref.entry
+    # structure
+    R = 16
+    deg = adj[:, 0]
+    assert adj.shape == (6000, R + 1) and deg.max() <= R
+    for u in range(0, 6000, 37):
+        row = adj[u, 1:1 + deg[u]]
+        assert len(set(row.tolist())) == len(row) and u not in row and (row < 6000).all()
+    assert st["mean_degree"] == pytest.approx(deg.mean())
+    assert reachable(adj, ix.entry_point) >= 0.99
+    # quality: Recall@10 at ef=64 close to the reference-built graph
+    gt = O.ref_brute_force_topk(ref.cold(), q, 10)
+    ids, _, _ = ix.search(q, 10, 64)
+    rids, _, _ = ref.run_query_batch(q, 64, 10, threads=4)
+    rec = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids, gt)])
+    rrec = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(rids, gt)])
+    assert rec >= rrec - 0.05, (rec, rrec)
+
+
+def test_build_is_deterministic_and_searchable():
+    base, q = mixture(3000, 64, 20, 0.35, seed=8, nq=50, sigma_mode="norm")
+    a, sa = build(base, m=6, ef_c=32, passes=2, batch=256)
+    b, sb = build(base, m=6, ef_c=32, passes=2, batch=256)
+    ca, aa, _ = a.export()
+    cb, ab, _ = b.export()
+    assert np.array_equal(aa, ab) and np.array_equal(ca, cb)
+    assert sa["batches"] == sb["batches"] > 0
+    ids, sc, cnt = a.search(q, 10, 32)
+    assert (cnt == 10).all()
+
+
+def test_build_rejects_bad_input():
+    x = np.ones((10, 8), np.float32)
+    x[3] = 0
+    with pytest.raises(Q.InvalidArgument):
+        build(x, m=2, ef_c=8)
+    with pytest.raises(Q.InvalidArgument):
+        build(np.ones((10, 8), np.float32), m=2, ef_c=8, alpha=0.5)
+
+
+@ref_only
+def test_gpu_graph_searches_identically_on_the_reference():
+    """The GPU-built graph is an ordinary qivr index: the reference's own
+    search over it returns exactly what the GPU search returns."""
+    base, q = mixture(4000, 128, 30, 0.35, seed=9, nq=100)
+    ix, _ = build(base, m=8, ef_c=32, passes=2, batch=512)
+    codes, adj, cold = ix.export()
+    ref = O.RefIndex.from_parts(codes, adj, cold, 128, 8, ix.entry_point)
+    for ef in (16, 64):
+        rids, rsc, _ = ref.run_query_batch(q, ef, 10, threads=4)
+        ids, sc, _ = ix.search(q, 10, ef)
+        assert np.array_equal(ids, rids)
+        assert np.array_equal(sc.view(np.uint32), rsc.view(np.uint32))

@@ -1,0 +1,97 @@
+"""Config-5 style build benchmark: GPU batched Vamana build vs the cached
+reference-built graph of the same seeded data.  Reports build seconds, degree
+stats and Recall@10 (fp32 brute-force GT on the GPU, 1000 queries) at the
+given ef for both graphs; saves the GPU graph to data_cache/ (builder=gpu).
+
+    python tools/build_bench.py --config 2 --passes 2 --out gpurun_out/build_cfg2.json
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--sigma-mode", default="literal")
+    ap.add_argument("--passes", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--ef", type=int, default=64)
+    ap.add_argument("--nq", type=int, default=1000)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    import torch
+
+    import paper_2605_02171_b200 as Q
+    from paper_2605_02171_b200 import datasets, graphs
+    cfg = datasets.CONFIGS[a.config]
+    base, queries = datasets.config_data(cfg, n=a.n, nq=a.nq, sigma_mode=a.sigma_mode)
+    n = base.shape[0]
+    st = {}
+    t0 = time.time()
+    ix = Q.GpuIndex.build(base, Q.BuildParams(m=cfg.m, ef_c=cfg.ef_c, alpha=cfg.alpha,
+                                              passes=a.passes, batch=a.batch), stats=st)
+    torch.cuda.synchronize()
+    wall = time.time() - t0
+    codes, adj, cold = ix.export()
+    path = graphs.graph_path(cfg, a.sigma_mode, n, builder="gpu")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez(path, adj=adj, entry=np.uint32(ix.entry_point), m=np.uint32(cfg.m),
+             ef_c=np.uint32(cfg.ef_c), alpha=np.float32(cfg.alpha),
+             digest=graphs.data_digest(base), build_seconds=np.float64(st["seconds"]))
+    # ground truth on the GPU (fp32, TF32 off) over the normalised store
+    torch.backends.cuda.matmul.allow_tf32 = False
+    qn, _, _ = Q.encode_queries(queries)
+    X = torch.from_numpy(cold).cuda()
+    qq = torch.from_numpy(qn).cuda()
+    best = None
+    for r0 in range(0, n, 131072):
+        s = qq @ X[r0:r0 + 131072].T
+        v, i = torch.topk(s, 10, dim=1)
+        i = i + r0
+        if best is None:
+            best = (v, i)
+        else:
+            cv = torch.cat([best[0], v], 1)
+            ci = torch.cat([best[1], i], 1)
+            vv, o = torch.topk(cv, 10, dim=1)
+            best = (vv, torch.gather(ci, 1, o))
+    gt = best[1].cpu().numpy()
+    del X
+
+    def recall(ids):
+        return float(np.mean([len(set(x.tolist()) & set(y.tolist())) / 10 for x, y in zip(ids, gt)]))
+
+    ids, _, _ = ix.search(queries, 10, a.ef)
+    out = {"config": a.config, "sigma_mode": a.sigma_mode, "n": n, "dim": cfg.dim,
+           "R": 2 * cfg.m, "L": cfg.ef_c, "passes": a.passes, "batch": a.batch,
+           "gpu_build_seconds": st["seconds"], "gpu_build_wall_seconds": wall,
+           "batches": st["batches"], "reprunes": st["reprunes"],
+           "degree": {"mean": st["mean_degree"], "min": st["min_degree"], "max": st["max_degree"]},
+           "entry_point": ix.entry_point, "recall_at_10_gpu_graph": recall(ids), "ef": a.ef}
+    g = graphs.load_graph(cfg, a.sigma_mode, n, base, builder="ref")
+    if g is not None:
+        rix = Q.GpuIndex.from_arrays(codes, g["adj"], cold, int(g["entry"]))
+        rids, _, _ = rix.search(queries, 10, a.ef)
+        deg = g["adj"][:, 0]
+        out.update(recall_at_10_ref_graph=recall(rids),
+                   ref_entry_point=int(g["entry"]),
+                   ref_degree={"mean": float(deg.mean()), "min": int(deg.min()), "max": int(deg.max())},
+                   ref_build_seconds=float(g.get("build_seconds", np.nan)),
+                   ref_build_threads=int(g.get("threads", 0)))
+    print(json.dumps(out))
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(json.dumps(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
