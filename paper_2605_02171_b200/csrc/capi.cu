@@ -248,7 +248,19 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     }
     cudaMemsetAsync(h->s_counter.p, 0, 64, s);  // work counter + flag word
     cudaEventRecord(h->ev[1], s);
-    if (mode.encode) {
+    // opt-in: the lane-0 FP64 chains stall the search warp; measured 3.10 ms
+    // fused vs 3.02 ms with the separate encode kernel (cfg2, 10k queries)
+    static const bool fused_env = [] {
+        const char* v = getenv("QVG_FUSED");
+        return v && v[0] == '1';
+    }();
+    const bool fused = mode.encode && fused_env && 4ull * ix.dim <= search_stage_bytes(ix);
+    if (fused) {
+        // K1 runs as the search kernel's per-query prologue
+        a.qraw = static_cast<const float*>(din);
+        a.qn_out = static_cast<float*>(h->s_qn.p);
+        a.qstatus = nullptr;
+    } else if (mode.encode) {
         launch_encode(static_cast<const float*>(din), nq, ix.dim, ix.Dp,
                       static_cast<float*>(h->s_qn.p), static_cast<uint4*>(h->s_qc.p), nullptr,
                       static_cast<int32_t*>(h->s_qst.p), d_flags, s);

@@ -105,6 +105,8 @@ struct SearchLaunch {
     uint32_t* qctr;
     unsigned long long* counter;
     uint32_t* flags;        // atomicOr(1 << QVG_Q_TIE_OVERFLOW) on overflow
+    const float* qraw;      // non-null: fused encode prologue (raw queries nq x dim);
+    float* qn_out;          //   writes normalised queries here, status to out_status
     uint32_t variant;       // A/B switches (QVG_VARIANT env): bit0 no rerank L2 prefetch,
                             // bit1 paired-half distance pass
     uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
@@ -116,6 +118,8 @@ struct SearchLaunch {
 // default visited-table size (log2 slots): the largest table (256..4096
 // slots, >= ef) among those that keep the maximum number of resident blocks
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device);
+// contiguous bytes of the search kernel's per-warp TMA stage (both halves)
+uint32_t search_stage_bytes(const DevIndex& ix);
 
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid,
                        PlanInfo* info = nullptr);

@@ -275,7 +275,89 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         if (qq >= a.nq) break;
         const uint64_t q = qq;
 
-        const int32_t qst = a.qstatus ? a.qstatus[q] : 0;
+        int32_t qst = 0;
+        if (a.qraw) {
+            // fused K1 (encode.cu semantics, bit-exact): the stage is idle
+            // between queries and holds the raw row; lane 0 runs the two
+            // index-ordered double reductions (vec_math.hpp:28-44,
+            // encoding.cpp:23-30); the rest is lane-parallel
+            float* row = reinterpret_cast<float*>(stage0);
+            const float* src = a.qraw + q * ix.dim;
+            const uint32_t dim = ix.dim;
+            bool fin = true;
+            for (uint32_t i = lane; i < dim; i += 32) {
+                const float v = __ldg(src + i);
+                fin &= isfinite(v);
+                row[i] = v;
+            }
+            fin = __all_sync(kFull, fin);
+            __syncwarp();
+            qst = fin ? QVG_Q_OK : QVG_Q_NONFINITE_COORD;
+            double inv_d = 0.0;
+            if (lane == 0 && qst == QVG_Q_OK) {
+                double acc = 0.0;
+                uint32_t i = 0;
+                for (; i + 8 <= dim; i += 8) {
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = row[i + u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = __fma_rn((double)v[u], (double)v[u], acc);
+                }
+                for (; i < dim; ++i) acc = __fma_rn((double)row[i], (double)row[i], acc);
+                const double nrm = __dsqrt_rn(acc);
+                if (!(nrm > 0.0) || isinf(nrm)) qst = QVG_Q_BAD_NORM;
+                else inv_d = __ddiv_rn(1.0, nrm);
+            }
+            qst = __shfl_sync(kFull, qst, 0);
+            const float inv = __double2float_rn(__shfl_sync(kFull, inv_d, 0));
+            bool yfin = true;
+            float* qout = a.qn_out + q * ix.Dp;
+            for (uint32_t i = lane; i < ix.Dp; i += 32) {
+                const float y = (i < dim && qst == QVG_Q_OK) ? __fmul_rn(row[i], inv) : 0.0f;
+                yfin &= isfinite(y);
+                if (i < dim) row[i] = y;
+                qout[i] = y;
+            }
+            yfin = __all_sync(kFull, yfin);
+            if (qst == QVG_Q_OK && !yfin) qst = QVG_Q_NONFINITE_CODE;
+            __syncwarp();
+            float tau_l = 0.0f;
+            if (lane == 0 && qst == QVG_Q_OK) {
+                double s = 0.0;
+                uint32_t i = 0;
+                for (; i + 8 <= dim; i += 8) {
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = row[i + u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, fabs((double)v[u]));
+                }
+                for (; i < dim; ++i) s = __dadd_rn(s, fabs((double)row[i]));
+                tau_l = __double2float_rn(__ddiv_rn(s, (double)dim));
+            }
+            const float tau = __shfl_sync(kFull, tau_l, 0);
+            for (uint32_t w = lane; w < W; w += 32) {
+                uint32_t p0 = 0, p1 = 0, s0 = 0, s1 = 0;
+                const uint32_t b0 = w * 64, lim = min(64u, dim - b0);
+                for (uint32_t b = 0; b < lim; ++b) {
+                    const float y = row[b0 + b];
+                    const uint32_t pb = y > 0.0f, sb = fabsf(y) > tau;
+                    if (b < 32) {
+                        p0 |= pb << b;
+                        s0 |= sb << b;
+                    } else {
+                        p1 |= pb << (b - 32);
+                        s1 |= sb << (b - 32);
+                    }
+                }
+                qc[w] = make_uint4(p0, p1, s0, s1);
+            }
+            if (qst != QVG_Q_OK && lane == 0 && a.flags) atomicOr(a.flags, 1u << qst);
+            __syncwarp();
+        } else {
+            qst = a.qstatus ? a.qstatus[q] : 0;
+        }
         if (qst != 0) {
             for (uint32_t i = lane; i < a.k; i += 32) {
                 if (a.out_ids) a.out_ids[q * a.k + i] = kSentinel;
@@ -298,7 +380,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
 
         // ---- per-query init --------------------------------------------------
         const long long t_start = clock64();  // phase timers (variant bit 4: debug)
-        for (uint32_t w = lane; w < W; w += 32) qc[w] = a.qcodes[q * W + w];
+        if (!a.qraw)
+            for (uint32_t w = lane; w < W; w += 32) qc[w] = a.qcodes[q * W + w];
         if (xbits) {
             uint4* xb4 = reinterpret_cast<uint4*>(xbits);
             for (uint64_t i = lane; i < a.exact_words / 4; i += 32) xb4[i] = make_uint4(0, 0, 0, 0);
@@ -906,6 +989,12 @@ static uint32_t max_dyn_smem(int device) {
 static bool allow_max_smem(void* fn, int device) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)max_dyn_smem(device)) == cudaSuccess;
+}
+
+uint32_t search_stage_bytes(const DevIndex& ix) {
+    const uint32_t rw = pow2ceil((ix.R + 31) / 32);
+    const uint32_t sr = stage_rows_for(ix.W, rw * 32, stage_half_bytes());
+    return 2u * (sr / 4u) * group_stride(ix.W);
 }
 
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device) {
