@@ -52,6 +52,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=1000)
     ap.add_argument("--visited-slots", type=int, default=0)
+    ap.add_argument("--rerank-depths", default="auto",
+                    help="GPU-only rerank-depth rows: 'auto' = config 4's ef x {ef, 2ef}, "
+                         "'none', or 'ef:depth,...'")
+    ap.add_argument("--batch-sizes", default="auto",
+                    help="latency regime: batch sizes to time per call ('auto' = config 3's "
+                         "{1,128,10000} when --config 3, 'none', or a list)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
 
@@ -268,9 +274,9 @@ def ours(args):
                              timing_only=1)
     import ctypes as C
 
-    def step_dev(efv=ef):
+    def step_dev(efv=ef, o=opts):
         st = N.qvg_stats()
-        rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr(), nq, k, efv, C.byref(opts),
+        rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr(), nq, k, efv, C.byref(o),
                                    ids_d.data_ptr(), sc_d.data_ptr(), cnt_d.data_ptr(),
                                    st_d.data_ptr(), None, None, None, None, C.byref(st))
         if rc:
@@ -361,6 +367,62 @@ def ours(args):
                           expansions_per_query=s_ex["stats"]["expansions"] / nq,
                           evals_per_query=s_ex["stats"]["dist_evals"] / nq))
 
+    # ---- rerank depth (config 4): share of the rerank in time and bytes ---------
+    depth_rows = []
+    if args.rerank_depths == "auto":
+        pairs = [(e, d) for e in cfg.efs for d in (e, 2 * e)] if args.config == 4 else []
+    elif args.rerank_depths == "none":
+        pairs = []
+    else:  # "ef:depth,ef:depth"
+        pairs = [tuple(int(v) for v in p.split(":")) for p in args.rerank_depths.split(",") if p]
+    for e, d in pairs:
+        o_d = N.qvg_search_opts(visited_slots=args.visited_slots, entry_point=N.SENTINEL,
+                                timing_only=1, rerank_depth=d)
+        o_nr = N.qvg_search_opts(visited_slots=args.visited_slots, entry_point=N.SENTINEL,
+                                 timing_only=1, no_rerank=1)
+        s_ex = ix.search_ex(queries, k=k, ef=e, exact_visited=True, pools=False, rerank_depth=d)
+        for _ in range(3):
+            step_dev(e, o_d)
+            step_dev(e, o_nr)
+        t_ms, _, km, _ = timed(lambda: step_dev(e, o_d), args.sweep_steps)
+        _, _, km_nr, _ = timed(lambda: step_dev(e, o_nr), args.sweep_steps)
+        b = algorithmic_bytes(s_ex["stats"], W, D, k, nq)
+        ka, kn = float(np.mean(km)), float(np.mean(km_nr))
+        depth_rows.append(dict(
+            ef=e, depth=d, qps=world * nq * args.sweep_steps / (t_ms / 1e3), kernel_ms=ka,
+            kernel_ms_no_rerank=kn, rerank_time_share=1.0 - kn / ka,
+            rerank_rows_per_query=s_ex["stats"]["cold_accesses"] / nq,
+            rerank_byte_share=s_ex["stats"]["cold_accesses"] * 4 * D / b,
+            gbs=b / (ka / 1e3) / 1e9, recall_at_10=recall_at_k(s_ex["ids"][:rq], gt, k)))
+
+    # ---- latency regime: per-call latency at small batch sizes (config 3) -------
+    lat = []
+    bss = ([1, 128, 10000] if args.config == 3 else []) if args.batch_sizes == "auto" else (
+        [] if args.batch_sizes == "none" else [int(x) for x in args.batch_sizes.split(",") if x])
+    for B in bss:
+        B = min(B, nq)
+        calls = max(20, min(200, 20000 // B))
+        times = []
+        for c in range(calls + 3):
+            off = (c * B) % max(1, nq - B + 1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = N.qvg_stats()
+            rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr() + off * D * 4, B, k, ef,
+                                       C.byref(opts), ids_d.data_ptr(), sc_d.data_ptr(),
+                                       cnt_d.data_ptr(), st_d.data_ptr(), None, None, None, None,
+                                       C.byref(st))
+            e1.record(stream)
+            if rc:
+                raise RuntimeError(N.last_error())
+            torch.cuda.synchronize()
+            if c >= 3:
+                times.append(e0.elapsed_time(e1))
+        times.sort()
+        lat.append(dict(batch=B, calls=calls, p50_ms=times[len(times) // 2],
+                        p99_ms=times[min(len(times) - 1, int(0.99 * len(times)))],
+                        qps=B * len(times) / (sum(times) / 1e3)))
+
     # ---- CPU baseline + full-size parity (rank 0, N=1) ------------------------
     cpu = None
     parity = None
@@ -421,7 +483,8 @@ def ours(args):
                      "evals_per_query_exact": ex["stats"]["dist_evals"] / nq,
                      "evals_per_query_lossy": lo["stats"]["dist_evals"] / nq,
                      "tie_overflows": ex["stats"]["tie_overflows"]},
-        "cpu_baseline": cpu, "parity": parity, "ef_sweep": sweep,
+        "cpu_baseline": cpu, "parity": parity, "ef_sweep": sweep, "batch_latency": lat,
+        "rerank_depth": depth_rows,
         "gpu_launches": 2 * args.steps, "clocks": clocks,
     }
     line = json.dumps(out)

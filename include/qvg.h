@@ -105,7 +105,12 @@ typedef struct qvg_search_opts {
     uint32_t entry_point;   /* UINT32_MAX: the index's entry point                   */
     uint32_t no_rerank;     /* 1: skip rerank (pool only)                            */
     uint32_t timing_only;   /* 1: stats carries device timings only (no counter D2H)  */
-    uint32_t reserved[2];
+    uint32_t rerank_depth;  /* 0 = ef (the reference).  Otherwise k <= depth <= 2*ef:
+                             * rerank the `depth` best (dist, id) keys among all
+                             * scored nodes.  GPU-only knob (BASELINE config 4), no
+                             * reference counterpart; depth <= ef reranks a pool
+                             * prefix. */
+    uint32_t reserved[1];
 } qvg_search_opts;
 
 const char* qvg_last_error(void);
@@ -155,7 +160,8 @@ qvg_status qvg_search(qvg_index* index, const float* queries, uint64_t nq, uint3
 
 /* qvg_search plus options, the pool (nq x ef ids / dists, ascending (dist,id),
  * padded with UINT32_MAX) and per-query counters (nq x 8 u32: expansions, tie
- * expansions, evals, in-pool drops, adjacency slots, pool size, max tie depth,
+ * expansions, evals, in-pool drops, adjacency slots, rows reranked (== pool
+ * size at the reference rerank depth or without rerank), max tie depth,
  * status).  Any output may be NULL. */
 qvg_status qvg_search_ex(qvg_index* index, const float* queries, uint64_t nq, uint32_t k,
                          uint32_t ef, const qvg_search_opts* opts, uint32_t* out_ids,

@@ -300,6 +300,8 @@ def _orc_lib():
                                       C.c_uint32, C.c_int, C.c_uint32, C.c_uint32, _u32p,
                                       _f32p, _u32p, _i32p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       _u64p]
+        L.orc_query_depth.argtypes = [C.POINTER(_OrcIndex), _f32p, C.c_uint64, C.c_uint32,
+                                      C.c_uint32, C.c_uint32, _u32p, _f32p, _u32p]
         L.orc_float_topk.argtypes = [_f32p, C.c_uint64, _f32p, C.c_uint64, C.c_uint32,
                                      C.c_uint32, _u32p]
         L.orc_robust_prune.argtypes = [C.POINTER(_OrcIndex), _u32p, _u32p, C.c_uint32,
@@ -391,6 +393,21 @@ class OracleIndex:
         if pools:
             out.update(pool_ids=pi, pool_dists=pd, pool_n=pn)
         return out
+
+    def query_depth(self, queries, ef, k, depth):
+        """Rerank the `depth` best BQ keys of every scored node (GPU-only rerank
+        depth knob; depth == ef is the reference query)."""
+        q = np.ascontiguousarray(queries, np.float32).reshape(-1, self.dim)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.uint32)
+        sc = np.empty((nq, k), np.float32)
+        cnt = np.empty(nq, np.uint32)
+        rc = _orc_lib().orc_query_depth(C.byref(self._s), q, nq, ef, k, depth, ids, sc, cnt)
+        if rc == 4:
+            raise ValueError("bad params: need ef >= k >= 1 and depth >= k")
+        if rc == 6:
+            raise AssertionError("pool is not the prefix of the scored keys")
+        return dict(ids=ids, scores=sc, count=cnt)
 
     def robust_prune(self, ids, dists, max_degree, alpha):
         ids = np.ascontiguousarray(ids, np.uint32)

@@ -544,6 +544,65 @@ int orc_query_batch(const orc_index* ix, const float* queries, uint64_t nq, uint
     return worst_rc;
 }
 
+/* ---- rerank depth (GPU-only knob, BASELINE config 4; no reference oracle) ----
+ * Definition: rerank the `depth` smallest (dist, id) keys among every node the
+ * search scored.  The final pool is exactly the ef smallest scored keys (a key
+ * left out of it was rejected or evicted while above the then-worst pool key,
+ * and the worst only falls), so depth <= ef reranks a pool prefix and
+ * depth == ef is the reference's query (search.cpp:138-142).  The dual-heap
+ * search runs with exact visited stamps, so the scored set is the stamped set. */
+static int u64_cmp(const void* pa, const void* pb) {
+    const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+int orc_query_depth(const orc_index* ix, const float* queries, uint64_t nq, uint32_t ef,
+                    uint32_t k, uint32_t depth, uint32_t* out_ids, float* out_scores,
+                    uint32_t* out_count) {
+    if (k < 1 || ef < k || depth < k) return ORC_BAD_PARAMS;
+    const uint32_t dim = ix->dim;
+    const size_t w = words_for_dim(dim);
+    orc_ctx* c = orc_ctx_new(ix->n);
+    float* qn = (float*)malloc(dim * sizeof(float));
+    uint64_t* code = (uint64_t*)malloc(2 * w * sizeof(uint64_t));
+    uint32_t* pid = (uint32_t*)malloc((size_t)(ef + 1) * sizeof(uint32_t));
+    uint32_t* pd = (uint32_t*)malloc((size_t)(ef + 1) * sizeof(uint32_t));
+    uint64_t* keys = (uint64_t*)malloc((size_t)ix->n * sizeof(uint64_t));
+    uint32_t* ids = (uint32_t*)malloc((size_t)ix->n * sizeof(uint32_t));
+    int worst_rc = ORC_OK;
+    for (uint64_t qi = 0; qi < nq; ++qi) {
+        for (uint32_t j = 0; j < k; ++j) {
+            out_ids[qi * k + j] = UINT32_MAX;
+            out_scores[qi * k + j] = NAN;
+        }
+        out_count[qi] = 0;
+        int rc = orc_encode_query(queries + qi * dim, dim, qn, code, NULL);
+        if (rc != ORC_OK) {
+            worst_rc = rc;
+            continue;
+        }
+        uint32_t np = 0;
+        orc_beam_search_heap(ix, c, code, ef, ix->entry, pid, pd, &np, NULL);
+        uint64_t ns = 0;
+        for (uint64_t v = 0; v < ix->n; ++v)
+            if (c->stamp[v] == c->epoch) keys[ns++] = mkkey(node_dist(ix, code, (uint32_t)v), (uint32_t)v);
+        qsort(keys, ns, sizeof(uint64_t), u64_cmp);
+        const uint64_t take = ns < depth ? ns : depth;
+        for (uint64_t i = 0; i < take; ++i) ids[i] = (uint32_t)keys[i];
+        for (uint32_t i = 0; i < np && i < take; ++i)
+            if (ids[i] != pid[i]) worst_rc = ORC_OVERFLOW; /* pool != scored prefix: bug */
+        out_count[qi] = orc_rerank(ix, ids, (uint32_t)take, qn, k, out_ids + qi * k, out_scores + qi * k);
+    }
+    free(qn);
+    free(code);
+    free(pid);
+    free(pd);
+    free(keys);
+    free(ids);
+    orc_ctx_free(c);
+    return worst_rc;
+}
+
 /* ---- exact float top-k (ground truth) ------------------------------------- */
 
 int orc_float_topk(const float* base, uint64_t n, const float* queries, uint64_t nq,

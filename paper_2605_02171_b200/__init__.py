@@ -225,14 +225,15 @@ class GpuIndex:
 
     def search_ex(self, queries, k=10, ef=64, visited_slots=0, tie_capacity=0,
                   exact_visited=False, entry_point=None, rerank=True, pools=True,
-                  counters=True, check=True):
-        """Everything: results, per-query status, pool (ids+dists), counters, stats."""
+                  counters=True, check=True, rerank_depth=0):
+        """Everything: results, per-query status, pool (ids+dists), counters, stats.
+        rerank_depth (GPU-only, 0 = ef): rerank the best `rerank_depth` scored keys."""
         q = _f32(queries, self.dim)
         nq = q.shape[0]
         opts = N.qvg_search_opts(visited_slots=visited_slots, tie_capacity=tie_capacity,
                                  exact_visited=int(exact_visited),
                                  entry_point=SENTINEL if entry_point is None else entry_point,
-                                 no_rerank=int(not rerank))
+                                 no_rerank=int(not rerank), rerank_depth=rerank_depth)
         ids = np.empty((nq, k), np.uint32)
         sc = np.empty((nq, k), np.float32)
         cnt = np.empty(nq, np.uint32)

@@ -49,7 +49,7 @@ class qvg_search_opts(C.Structure):
     _fields_ = [("visited_slots", C.c_uint32), ("tie_capacity", C.c_uint32),
                 ("exact_visited", C.c_uint32), ("entry_point", C.c_uint32),
                 ("no_rerank", C.c_uint32), ("timing_only", C.c_uint32),
-                ("reserved", C.c_uint32 * 2)]
+                ("rerank_depth", C.c_uint32), ("reserved", C.c_uint32 * 1)]
 
 
 class qvg_build_params(C.Structure):
@@ -71,10 +71,12 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
+    global LIB_PATH
+    LIB_PATH = os.environ.get("QVG_LIB", LIB_PATH)  # A/B of two builds (tools/)
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: the B200 query path has no CPU fallback. "
-            "Build it with `python -m paper_2605_02171_b200.build`.")
+            "Build it with `python paper_2605_02171_b200/build.py`.")
     L = C.CDLL(LIB_PATH)
     vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
     L.qvg_last_error.restype = C.c_char_p

@@ -1,6 +1,6 @@
 """Build libqvg.so (sm_100a CUDA + host C++) in-tree with nvcc.
 
-``python -m paper_2605_02171_b200.build`` or ``__graft_entry__.build()``.
+``python paper_2605_02171_b200/build.py`` or ``__graft_entry__.build()``.
 Objects go to build/, the shared library next to this file so it travels to
 the GPU box with the repo snapshot.  ptxas register/smem reports are kept in
 build/ptxas.log.

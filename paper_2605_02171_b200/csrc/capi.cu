@@ -145,22 +145,30 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     }
     uint32_t tcap = opts && opts->tie_capacity ? opts->tie_capacity : (ef < 64 ? 64u : ef);
     tcap = (tcap + 3) & ~3u;
+    const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
+    // rerank depth (GPU-only knob): 0 = ef, the reference
+    const uint32_t depth = opts && opts->rerank_depth ? opts->rerank_depth : ef;
+    if (mode.rerank && (depth < k || depth > 2 * ef)) {
+        set_error("search: rerank_depth must satisfy k <= rerank_depth <= 2*ef");
+        return QVG_INVALID_ARGUMENT;
+    }
+    const uint32_t xa = do_rerank ? extra_depth(ef, depth) : 0u;
     uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
     uint32_t vlog;
-    auto cached = h->plans.find(qvg_index::PlanKey{ef, tcap, vslots});
+    auto cached = h->plans.find(qvg_index::PlanKey{ef, tcap, vslots, xa});
     if (cached != h->plans.end()) {
         vlog = cached->second.first;
     } else if (vslots) {
-        if (vslots < 32 * ((ef + 31) / 32)) vslots = 32 * ((ef + 31) / 32);  // scores alias it
+        const uint32_t floor_slots = 32 * ((ef + xa + 31) / 32);  // rerank scores alias it
+        if (vslots < floor_slots) vslots = floor_slots;
         vlog = log2_floor(vslots);
         if ((1u << vlog) < vslots) ++vlog;
         if (vlog < 5) vlog = 5;
     } else {
         // largest table that keeps the most resident warps (occupancy-aware)
-        vlog = auto_visited_log2(ix, ef, tcap, h->device);
+        vlog = auto_visited_log2(ix, ef, tcap, h->device, xa);
     }
     const bool exact = opts && opts->exact_visited;
-    const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
     const bool want_ctr = out_qctr != nullptr || (stats && !(opts && opts->timing_only));
 
     qvg_status st = QVG_OK;
@@ -195,6 +203,8 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     a.vis_log2 = vlog;
     a.tie_cap = tcap;
     a.do_rerank = do_rerank;
+    a.depth = ef + xa;
+    if (do_rerank && depth < ef) a.depth = depth;
     a.out_ids = static_cast<uint32_t*>(o_ids.dev);
     a.out_scores = static_cast<float*>(o_sc.dev);
     a.out_count = static_cast<uint32_t*>(o_cnt.dev);
@@ -217,7 +227,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     PlanInfo pinfo;
     {
         const uint32_t vreq = opts && opts->visited_slots ? opts->visited_slots : 0u;
-        const qvg_index::PlanKey key{ef, tcap, vreq};
+        const qvg_index::PlanKey key{ef, tcap, vreq, xa};
         auto it = h->plans.find(key);
         if (it == h->plans.end()) {
             if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;

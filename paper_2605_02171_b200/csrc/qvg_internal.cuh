@@ -60,11 +60,13 @@ struct qvg_index {
     // {2W, 1}) for tile::gather4; valid iff has_tmap (W <= 128)
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
-    // launch plans keyed by (ef, tie capacity, visited-slot request)
+    // launch plans keyed by (ef, tie capacity, visited-slot request, extra depth)
     struct PlanKey {
-        uint32_t ef, tcap, vreq;
+        uint32_t ef, tcap, vreq, xa;
         bool operator<(const PlanKey& o) const {
-            return ef != o.ef ? ef < o.ef : (tcap != o.tcap ? tcap < o.tcap : vreq < o.vreq);
+            if (ef != o.ef) return ef < o.ef;
+            if (tcap != o.tcap) return tcap < o.tcap;
+            return vreq != o.vreq ? vreq < o.vreq : xa < o.xa;
         }
     };
     std::map<PlanKey, std::pair<uint32_t, qvg::PlanInfo>> plans;  // -> (vis_log2, info)
@@ -111,13 +113,19 @@ struct SearchLaunch {
                             // bit1 paired-half distance pass
     uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
     uint64_t exact_words;   // words per slot
+    uint32_t depth;         // rerank depth (>= k): the `depth` best scored keys are
+                            // reranked; depth == ef is the reference (search.cpp:138)
 };
+
+// keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)
+__host__ __device__ inline uint32_t extra_depth(uint32_t ef, uint32_t depth) { return depth > ef ? depth - ef : 0u; }
 
 // grid = min(resident blocks, ceil(nq / warps per block)); exact-visited
 // bitmaps are sized for grid * kWarpsPerBlock warp slots.
 // default visited-table size (log2 slots): the largest table (256..4096
 // slots, >= ef) among those that keep the maximum number of resident blocks
-uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device);
+uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
+                           uint32_t xa = 0);
 // contiguous bytes of the search kernel's per-warp TMA stage (both halves)
 uint32_t search_stage_bytes(const DevIndex& ix);
 

@@ -140,7 +140,8 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
 }
 
 struct SmemLayout {
-    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, qsl, total;
+    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, qsl, acd, axk,
+        axr, total;
 };
 
 // bytes of one 4-row TMA group in the stage; gather4 destinations must be
@@ -150,9 +151,11 @@ __host__ __device__ inline uint32_t group_stride(uint32_t W) { return (64u * W +
 
 // Per-warp shared-memory carve-up (bytes).  Stage halves are 128-B aligned
 // (TMA destinations); the total is a multiple of 128 so every warp's base is.
+// EFM = pool + extra-depth capacity rounded to 32; xa > 0 adds the extra-depth
+// candidate buffers.
 __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uint32_t W,
                                                   uint32_t tie_cap, uint32_t vis_slots,
-                                                  uint32_t stage_rows) {
+                                                  uint32_t stage_rows, uint32_t xa = 0) {
     SmemLayout L;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -164,7 +167,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.bars = take(16, 16);
     L.stage0 = take((stage_rows / 4) * group_stride(W), 128);
     L.stage1 = take((stage_rows / 4) * group_stride(W), 128);
-    L.pk = take(8 * EFM, 16);    // pool keys
+    L.pk = take(8 * EFM, 16);    // pool keys P[0, ef), then extra-depth keys A
     L.ctd = take(8 * RM, 16);    // contenders, row order
     L.evk = L.ctd;               // keys evicted this step (ctd is dead by then)
     L.crp = take(4 * RM, 16);    // contender rank in P, row order
@@ -175,6 +178,12 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.tie = take(4 * tie_cap, 16);
     L.vis = take(4 * vis_slots, 16);  // rerank scores alias this region (vis_slots >= EFM)
     L.qsl = take(2 * 48 * 4, 16);     // rerank query slices (one per stage half)
+    // extra depth: A candidates of one step (<= RM: each scored key is a P
+    // contender or an A candidate, and evictions <= P contenders), sorted copy
+    // and their ranks in A
+    L.acd = take(xa ? 8 * RM : 0, 16);
+    L.axk = take(xa ? 8 * RM : 0, 16);
+    L.axr = take(xa ? 4 * RM : 0, 16);
     L.total = (o + 127u) & ~127u;
     return L;
 }
@@ -197,7 +206,16 @@ struct MinBlocks {
     static constexpr int value = RW == 1 ? 9 : (RW == 2 ? 7 : 5);
 };
 
-template <int RW>
+// XA: rerank deeper than ef.  A = the best `xa` scored keys outside P, kept
+// sorted at pk[ef, ef + na): every A key exceeds max(P) (it was rejected or
+// evicted while above the then-worst pool key, and the worst only falls), so
+// pk[0, np + na) is the sorted list of the best scored keys.  A takes the
+// step's non-contenders below max(A) and the keys leaving P; the search itself
+// (pick, stop test, tie stack) never reads A.
+// SPLIT: several lanes per scored row (wide rows, few rows per stage half); a
+// separate instantiation because the extra loop costs the narrow-row kernels
+// ~1.5% even when unused (cfg2 A/B, tools/tune_search.py).
+template <int RW, bool XA, bool SPLIT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
@@ -213,8 +231,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     const uint32_t gstride = group_stride(W);  // bytes per 4-row TMA group (128-B aligned)
     const uint32_t VS = 1u << a.vis_log2;
     const uint32_t ef = a.ef;
-    const uint32_t EFM = (ef + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR);
+    const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
+    const uint32_t EFM = (ef + xa + 31u) & ~31u;
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -231,10 +250,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
     float* qsl = reinterpret_cast<float*>(base + L.qsl);
+    uint64_t* acd = reinterpret_cast<uint64_t*>(base + L.acd);
+    uint64_t* axk = reinterpret_cast<uint64_t*>(base + L.axk);
+    uint32_t* axr = reinterpret_cast<uint32_t*>(base + L.axr);
+    uint64_t* pa = pk + ef;  // A
 
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
     uint32_t* xbits = a.exact_bits ? a.exact_bits + gwarp * a.exact_words : nullptr;
     const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
+    // lanes per scored row: the largest power of two with LPR * SR <= 32
+    uint32_t lpr_log = 0;
+    while (SPLIT && (SR << (lpr_log + 1)) <= 32u) ++lpr_log;
+    const uint32_t LPR = SPLIT ? 1u << lpr_log : 1u;
 
     if (lane == 0) {
         mbar_init(&bars[0]);
@@ -395,6 +422,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             else vis[vhash(entry, a.vis_log2)] = entry;
         }
         uint32_t np = 0, tn = 0, tdist = 0, hint = 0;
+        uint32_t na = 0;  // |A| (XA only)
         uint32_t c_exp = 0, c_tie = 0, c_eval = 0, c_drop = 0, c_slots = 0, c_maxtie = 0;
         bool overflow = false;
         uint32_t n = 1;  // rows to score in cid[0..n)
@@ -449,7 +477,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             }
             // (b) SM2 distances lane-per-row from the stage; contenders -> ctd/crp
             const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
-            uint32_t m = 0;
+            const uint64_t worst_a = (XA && na == xa) ? pa[xa - 1] : kInfKey;
+            uint32_t m = 0, ma = 0;
             // contender test + row-order compaction of one scored row per lane
             auto emit = [&](bool valid, uint32_t d, uint32_t id) {
                 const uint64_t key = mkkey(d, id);
@@ -469,6 +498,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     crp[pos] = rp;
                 }
                 m += __popc(bal);
+                if constexpr (XA) {
+                    // above max(P) (key == max(P) is P's own entry) and below
+                    // max(A); a key already in A is a visited-table miss
+                    bool ac = valid && np == ef && key > worst && key < worst_a;
+                    if (ac) {
+                        const uint32_t r = lower_bound_key(pa, na, key);
+                        ac = !(r < na && pa[r] == key);
+                    }
+                    const unsigned ba = __ballot_sync(kFull, ac);
+                    if (ac) acd[ma + __popc(ba & lt_mask)] = key;
+                    ma += __popc(ba);
+                }
             };
             // paired pass (wait for both halves, then score 2 rows per lane) is
             // opt-in: measured slower than overlapping half-0 scoring with the
@@ -531,7 +572,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 const uint32_t r0 = k * SR;
                 const uint32_t cnt = min(n - r0, SR);
                 const uint4* st = reinterpret_cast<const uint4*>(stage0 + h * stage_delta);
-                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+                // LPR lanes per row (wide rows leave a half with < 32 rows): part
+                // p of row r reads chunks (lane + LPR*i) mod W, i.e. offsets
+                // p, p+LPR, ... from the row's rotation LPR*r — every chunk once,
+                // and the 8 lanes of an LDS.128 phase hit distinct bank quads
+                for (uint32_t i0 = 0; LPR == 1u && i0 < cnt; i0 += 32) {
                     const uint32_t j = i0 + lane;
                     const bool valid = j < cnt;
                     uint32_t d = 0;
@@ -545,6 +590,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                         }
                     }
                     emit(valid, d, valid ? cid[r0 + j] : kSentinel);
+                }
+                for (uint32_t i0 = 0; LPR > 1u && i0 < cnt; i0 += 32u >> lpr_log) {
+                    const uint32_t j = i0 + (lane >> lpr_log);
+                    const uint32_t part = lane & (LPR - 1u);
+                    const bool valid = j < cnt;
+                    uint32_t d = 0;
+                    if (valid) {
+                        const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
+                        uint32_t cc = rot;
+#pragma unroll 4
+                        for (uint32_t t = part; t < W; t += LPR) {
+                            d += sm2_chunk(qc[cc], rowp[cc]);
+                            cc += LPR;
+                            if (cc >= W) cc -= W;
+                        }
+                    }
+                    for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
+                    const bool lead = valid && part == 0;
+                    emit(lead, d, lead ? cid[r0 + j] : kSentinel);
                 }
                 if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), h);
             }
@@ -640,9 +704,51 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                         tn += put;
                         if (tn > c_maxtie) c_maxtie = tn;
                     }
+                    if constexpr (XA) {  // keys leaving P (rejected or evicted) -> A candidates
+                        for (uint32_t e = lane; e < nev; e += 32) acd[ma + e] = ordk(evk[e]);
+                        ma += nev;
+                    }
                 }
                 np = total < ef ? total : ef;
                 __syncwarp();
+            }
+            if constexpr (XA) {
+                if (ma > 0) {
+                    // merge the step's candidates into A (ascending, capped at xa):
+                    // candidate i (key order) lands at rankA(i) + i; A[idx] moves
+                    // right by #{candidates with rankA <= idx}
+                    __syncwarp();
+                    for (uint32_t i = lane; i < ma; i += 32) {
+                        const uint64_t x = acd[i];
+                        uint32_t rx = 0;
+                        for (uint32_t j = 0; j < ma; ++j) rx += acd[j] < x;
+                        axk[rx] = x;
+                        axr[rx] = lower_bound_key(pa, na, x);
+                    }
+                    __syncwarp();
+                    const uint32_t lo = axr[0];
+                    if (lo < na) {
+                        for (int cb = (int)((na - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
+                            const uint32_t idx = (uint32_t)cb + lane;
+                            const bool mv = idx < na && idx >= lo;
+                            uint64_t p = 0;
+                            uint32_t npos = 0;
+                            if (mv) {
+                                p = pa[idx];
+                                npos = idx + upper_bound_u32(axr, ma, idx);
+                            }
+                            __syncwarp();
+                            if (mv && npos < xa) pa[npos] = p;
+                            __syncwarp();
+                        }
+                    }
+                    for (uint32_t i = lane; i < ma; i += 32) {
+                        const uint32_t npos = axr[i] + i;
+                        if (npos < xa) pa[npos] = axk[i];
+                    }
+                    na = na + ma < xa ? na + ma : xa;
+                    __syncwarp();
+                }
             }
 
             // (f) pick: first unexpanded pool entry at or after the hint, else
@@ -762,6 +868,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             }
         }
         if (a.do_rerank) {
+            // rerank the NR best scored keys pk[0, NR) (P, then A when XA)
+            const uint32_t NR = min(np + na, a.depth);
+            if (lane == 0 && a.qctr && NR != np) a.qctr[q * 8 + 5] = NR;  // rows reranked
             // rerank: one lane per pool entry, 4 sequential double chains
             const float* qv = a.qn + q * ix.Dp;
             __syncwarp();
@@ -774,11 +883,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 const uint32_t dim = ix.dim;
                 const uint32_t main4 = dim & ~3u;
                 const uint32_t nsl = (dim + SL - 1) / SL;
-                const uint32_t rounds = ((np + 31) / 32) * nsl;
+                const uint32_t rounds = ((NR + 31) / 32) * nsl;
                 const uint32_t cgs = (16u * SL + 127u) & ~127u;  // bytes per 4-row group
                 auto rr_issue = [&](uint32_t t) {
                     const uint32_t g = t / nsl, s = t % nsl, h = t & 1u;
-                    const uint32_t rows = min(32u, np - 32u * g);
+                    const uint32_t rows = min(32u, NR - 32u * g);
                     const uint32_t ng4 = (rows + 3u) >> 2;
                     // the query slice rides in the same transaction (16-B multiple,
                     // clipped to the padded row so the last query never overreads)
@@ -821,7 +930,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     }
                     if (s == 0) s0 = s1 = s2 = s3 = 0.0;
                     const uint32_t row = 32u * g + lane;
-                    if (row < np) {
+                    if (row < NR) {
                         const float4* rp = reinterpret_cast<const float4*>(
                             stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
 #pragma unroll
@@ -849,9 +958,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             } else {
                 // fallback: one lane per pool entry streaming its row from global
                 if (!(a.variant & 1u))
-                    for (uint32_t idx = lane; idx < np; idx += 32)
+                    for (uint32_t idx = lane; idx < NR; idx += 32)
                         prefetch_l2(ix.cold + (size_t)(uint32_t)pk[idx] * ix.Dp, ix.Dp * 4u);
-                for (uint32_t idx = lane; idx < np; idx += 32) {
+                for (uint32_t idx = lane; idx < NR; idx += 32) {
                     const uint32_t id = (uint32_t)pk[idx];
                     const float* row = ix.cold + (size_t)id * ix.Dp;
                     sc[idx] = (a.variant & 4u) ? dot4_exact<true>(qv, row, ix.dim)
@@ -865,11 +974,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 a.qctr[q * 8 + 1] = (uint32_t)((t_dots - t_search) >> 4);
             }
             // rank by (score desc, id asc) and emit the first k
-            for (uint32_t idx = lane; idx < np; idx += 32) {
+            for (uint32_t idx = lane; idx < NR; idx += 32) {
                 const float si = sc[idx];
                 const uint32_t ii = (uint32_t)pk[idx];
                 uint32_t rank = 0;
-                for (uint32_t j = 0; j < np; ++j) {
+                for (uint32_t j = 0; j < NR; ++j) {
                     const float sj = sc[j];
                     const uint32_t ij = (uint32_t)pk[j];
                     rank += (sj > si) | ((sj == si) & (ij < ii));
@@ -879,11 +988,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     a.out_scores[q * a.k + rank] = si;
                 }
             }
-            for (uint32_t r = np + lane; r < a.k; r += 32) {
+            for (uint32_t r = NR + lane; r < a.k; r += 32) {
                 a.out_ids[q * a.k + r] = kSentinel;
                 a.out_scores[q * a.k + r] = __int_as_float(0x7fc00000);
             }
-            if (lane == 0 && a.out_count) a.out_count[q] = np < a.k ? np : a.k;
+            if (lane == 0 && a.out_count) a.out_count[q] = NR < a.k ? NR : a.k;
             if ((a.variant & 16u) && lane == 0 && a.qctr)
                 a.qctr[q * 8 + 2] = (uint32_t)((clock64() - t_dots) >> 4);
         }
@@ -924,15 +1033,33 @@ struct Plan {
     uint32_t rw, SR, warp_bytes, block_bytes;
 };
 
-Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap) {
+// split rows over lanes when a stage half holds at most this many rows
+// (QVG_SPLIT_MAX_ROWS; 0 = never)
+uint32_t split_max_rows() {
+    static uint32_t v = [] {
+        const char* e = getenv("QVG_SPLIT_MAX_ROWS");
+        return e ? (uint32_t)atol(e) : 8u;
+    }();
+    return v;
+}
+
+template <int RW>
+void* pick_kernel(bool xa, bool split) {
+    if (xa) return split ? (void*)search_kernel<RW, true, true> : (void*)search_kernel<RW, true, false>;
+    return split ? (void*)search_kernel<RW, false, true> : (void*)search_kernel<RW, false, false>;
+}
+
+Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap,
+               uint32_t xa) {
     Plan p;
     p.rw = pow2ceil((ix.R + 31) / 32);
-    if (p.rw == 1) p.fn = (void*)search_kernel<1>;
-    else if (p.rw == 2) p.fn = (void*)search_kernel<2>;
-    else p.fn = (void*)search_kernel<4>;
     p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
-    const SmemLayout L =
-        smem_layout((ef + 31) & ~31u, p.rw * 32, ix.W, tie_cap, 1u << vis_log2, p.SR);
+    const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
+    if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
+    else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
+    else p.fn = pick_kernel<4>(xa != 0, split);
+    const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
+                                     1u << vis_log2, p.SR, xa);
     p.warp_bytes = L.total;
     p.block_bytes = p.warp_bytes * kWarpsPerBlock;
     return p;
@@ -997,13 +1124,14 @@ uint32_t search_stage_bytes(const DevIndex& ix) {
     return 2u * (sr / 4u) * group_stride(ix.W);
 }
 
-uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device) {
+uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
+                           uint32_t xa) {
     uint32_t min_log = 8;  // 256 slots
-    while ((1u << min_log) < ((ef + 31u) & ~31u)) ++min_log;
+    while ((1u << min_log) < ((ef + xa + 31u) & ~31u)) ++min_log;  // rerank scores alias it
     uint32_t best_log = min_log;
     int best_blocks = -1;
     for (uint32_t lg = min_log; lg <= 12 || lg == min_log; ++lg) {
-        const Plan p = make_plan(ix, ef, lg, tie_cap);
+        const Plan p = make_plan(ix, ef, lg, tie_cap, xa);
         if (p.block_bytes > max_dyn_smem(device) || !allow_max_smem(p.fn, device)) {
             break;
         }
@@ -1023,7 +1151,12 @@ uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, in
 }
 
 qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, PlanInfo* info) {
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
+    const uint32_t xa = extra_depth(a.ef, a.depth);
+    if ((1u << a.vis_log2) < ((a.ef + xa + 31u) & ~31u)) {
+        set_error("search: visited_slots must be >= ef + extra rerank depth (rounded to 32)");
+        return QVG_INVALID_ARGUMENT;
+    }
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa);
     if (p.block_bytes > max_dyn_smem(device)) {
         set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
         return QVG_INVALID_ARGUMENT;
@@ -1055,7 +1188,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
 
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s) {
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth));
     alignas(64) CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
     const CUtensorMap* m = tmap ? tmap : &dummy;

@@ -96,6 +96,70 @@ def test_golden_pools_ids_scores(name):
 
 
 @pytest.mark.parametrize("name", ["g1", "g2", "g3"])
+def test_rerank_depth_vs_oracle(name):
+    """Config-4 rerank depth (GPU-only knob): rerank the `depth` best scored
+    keys.  Bit-exact against orc_query_depth for depth in {k, ef/2, ef, 2ef},
+    with the default and a tiny (lossy) visited table; the pool is unchanged."""
+    g = load_golden(name)
+    ix = gpu_index_from_golden(g)
+    orc = O.OracleIndex(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    k = int(g["k"])
+    for ef in g["efs"]:
+        ef = int(ef)
+        for depth in sorted({k, max(k, ef // 2), ef, 2 * ef}):
+            o = orc.query_depth(g["queries"], ef, k, depth)
+            for vslots in (0, 32):
+                r = ix.search_ex(g["queries"], k=k, ef=ef, visited_slots=vslots,
+                                 rerank_depth=depth)
+                assert np.array_equal(r["ids"], o["ids"]), (name, ef, depth, vslots)
+                assert np.array_equal(r["scores"].view(np.uint32), o["scores"].view(np.uint32))
+                assert np.array_equal(r["count"], o["count"])
+                assert np.array_equal(r["pool_ids"], g[f"pool_ids_{ef}"])
+    with pytest.raises(Q.InvalidArgument, match="rerank_depth"):
+        ix.search_ex(g["queries"], k=k, ef=int(g["efs"][-1]), rerank_depth=2 * int(g["efs"][-1]) + 1)
+    assert k > 1
+    with pytest.raises(Q.InvalidArgument, match="rerank_depth"):
+        ix.search_ex(g["queries"], k=k, ef=int(g["efs"][-1]), rerank_depth=k - 1)
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [{root!r}, {tests!r}]
+from conftest import load_golden
+import paper_2605_02171_b200 as Q
+for name in ("g1", "g2", "g3"):
+    g = load_golden(name)
+    ix = Q.GpuIndex.from_arrays(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    for ef in g["efs"]:
+        ef = int(ef)
+        r = ix.search_ex(g["queries"], k=int(g["k"]), ef=ef)
+        assert np.array_equal(r["ids"], g["ids_%d" % ef]), (name, ef)
+        assert np.array_equal(r["scores"].view(np.uint32), g["scores_%d" % ef]), (name, ef)
+        assert np.array_equal(r["pool_ids"], g["pool_ids_%d" % ef]), (name, ef)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("env", [{"QVG_FUSED": "1"}, {"QVG_ENCODE": "1"}, {"QVG_ENCODE": "3"},
+                                 {"QVG_VARIANT": "2"}, {"QVG_VARIANT": "8"},
+                                 {"QVG_VARIANT": "13"}, {"QVG_STAGE_HALF_BYTES": "512"},
+                                 {"QVG_SPLIT_MAX_ROWS": "32"},
+                                 {"QVG_SPLIT_MAX_ROWS": "32", "QVG_STAGE_HALF_BYTES": "512"},
+                                 {"QVG_SPLIT_MAX_ROWS": "0"}])
+def test_opt_in_variants_match_golden(env):
+    """The opt-in kernel variants (env switches read once per process): fused
+    encode prologue, tiled / block encoders, paired distance pass, LDG rerank
+    fallback (+ no-allocate loads, no L2 prefetch), tiny stage.  All bit-exact."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    script = _VARIANT_SCRIPT.format(root=os.path.dirname(here), tests=here)
+    r = subprocess.run([sys.executable, "-c", script], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name", ["g1", "g2", "g3"])
 def test_exact_visited_mode_matches_oracle_counters(name):
     g = load_golden(name)
     ix = gpu_index_from_golden(g)
@@ -302,3 +366,10 @@ def test_cfg1_shape_parity_vs_reference(sigma_mode):
         assert np.array_equal(r["ids"], ids), ef
         assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32)), ef
         assert r["stats"]["tie_overflows"] == 0
+    # rerank depth 2*ef (config 4's GPU-only knob) against the C restatement
+    orc = O.OracleIndex.from_ref(ref)
+    for ef in (16, 64):
+        o = orc.query_depth(q, ef, 10, 2 * ef)
+        r = ix.search_ex(q, k=10, ef=ef, rerank_depth=2 * ef)
+        assert np.array_equal(r["ids"], o["ids"]), ef
+        assert np.array_equal(r["scores"].view(np.uint32), o["scores"].view(np.uint32)), ef

@@ -111,6 +111,26 @@ def test_oracle_reproduces_golden(name, mode):
         assert r["stats"]["tie_overflows"] == 0
 
 
+@pytest.mark.parametrize("name", ["g1", "g2", "g3"])
+def test_oracle_rerank_depth(name):
+    """Rerank-depth knob (config 4, GPU-only): depth == ef is the golden query;
+    the pool is always the prefix of the sorted scored keys (checked inside
+    orc_query_depth); a deeper rerank never loses a better-scored pool hit."""
+    g = load_golden(name)
+    ix = O.OracleIndex(g["codes"], g["adj"], g["cold"], int(g["entry"]))
+    k = int(g["k"])
+    for ef in g["efs"]:
+        ef = int(ef)
+        r = ix.query_depth(g["queries"], ef, k, ef)
+        assert np.array_equal(r["ids"], g[f"ids_{ef}"])
+        assert np.array_equal(r["scores"].view(np.uint32), g[f"scores_{ef}"])
+        r2 = ix.query_depth(g["queries"], ef, k, 2 * ef)
+        # top-1 score over a superset can only improve
+        ok = r["count"] > 0
+        assert np.all(r2["scores"][ok, 0] >= r["scores"][ok, 0])
+        assert np.all(r2["count"] >= r["count"])
+
+
 def test_oracle_float_topk_matches_golden_gt():
     g = load_golden("g1")
     gt = O.orc_float_topk(g["cold"], g["queries"], 10)
