@@ -1034,11 +1034,12 @@ struct Plan {
 };
 
 // split rows over lanes when a stage half holds at most this many rows
-// (QVG_SPLIT_MAX_ROWS; 0 = never)
+// (QVG_SPLIT_MAX_ROWS; 0 = never).  cfg3 (16 rows/half): 6.38 -> 5.62 ms;
+// cfg4 (8 rows/half): 18.8 -> 9.9 ms; cfg1/cfg2 (32 rows/half): not split.
 uint32_t split_max_rows() {
     static uint32_t v = [] {
         const char* e = getenv("QVG_SPLIT_MAX_ROWS");
-        return e ? (uint32_t)atol(e) : 8u;
+        return e ? (uint32_t)atol(e) : 16u;
     }();
     return v;
 }

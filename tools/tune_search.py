@@ -28,6 +28,13 @@ def child(a):
     cfg = datasets.CONFIGS[a.config]
     base, queries = datasets.config_data(cfg, nq=a.nq, sigma_mode=a.sigma_mode)
     g = graphs.load_graph(cfg, a.sigma_mode, base.shape[0], base)
+    if g is None:
+        g = graphs.load_graph(cfg, a.sigma_mode, base.shape[0], base, builder="gpu")
+    if g is None:  # no cached graph: build on the GPU (seconds)
+        bi = Q.GpuIndex.build(base, Q.BuildParams(m=cfg.m, ef_c=cfg.ef_c, alpha=cfg.alpha))
+        _, adj, _ = bi.export()
+        g = dict(adj=adj, entry=bi.entry_point)
+        bi.close()
     qn, codes, _ = Q.encode_queries(base)
     ix = Q.GpuIndex.from_arrays(codes, g["adj"], qn, int(g["entry"]))
     del qn, codes
