@@ -33,6 +33,10 @@
  *   qvg_build             qivr::build_index (builder.cpp:137-155) — GPU batched
  *                         BQ-space Vamana insertion with RobustPrune
  *                         (graph.hpp:162-227)
+ *   qvg_brute_force_topk  qivr::brute_force_topk (eval.hpp:19-21,
+ *                         eval.cpp:81-168) — exact ground truth on the GPU
+ *   qvg_compatibility_probe  qivr::compatibility_probe (eval.cpp:196-222)
+ *   qvg_strong_bit_rate   qivr::strong_bit_rate (encoding.cpp:132-167)
  *
  * Error mapping: QVG_INVALID_ARGUMENT <-> std::invalid_argument
  * (SearchParams::validate search.hpp:16-19; dim mismatch search.cpp:125-127;
@@ -211,6 +215,56 @@ typedef struct qvg_build_stats {
 
 qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim, const qvg_build_params* p,
                      int device, qvg_index** out, qvg_build_stats* stats);
+
+/* ---- evaluation support ------------------------ */
+
+/* Scorers of qivr::Scorer (eval.hpp:13). */
+#define QVG_SCORER_FLOAT_COSINE 0
+#define QVG_SCORER_SM2 1
+#define QVG_SCORER_SIGN1 2
+#define QVG_SCORER_SQ2 3 /* not implemented on the GPU (QVG_NOT_IMPLEMENTED) */
+
+/* qivr::brute_force_topk (eval.hpp:19-21, eval.cpp:81-168): exact top-k of
+ * every base row per query.  float_cosine ranks dot_f32 (the 4-chain double
+ * dot) descending; sm2 / sign1 rank the raw codes' distances ascending; ties
+ * by ascending id; exclude_identity skips row j == query index.  base n x dim,
+ * queries nq x dim (host or device).  out_ids nq x k (rows shorter than k
+ * padded with UINT32_MAX); out_scores (float_cosine) / out_dists (code
+ * scorers) / out_count nullable.  k <= 256. */
+qvg_status qvg_brute_force_topk(int device, const float* base, uint64_t n, const float* queries,
+                                uint64_t nq, uint32_t dim, uint32_t k, int scorer,
+                                int exclude_identity, uint32_t* out_ids, float* out_scores,
+                                uint32_t* out_dists, uint32_t* out_count);
+
+/* qivr::ProbeReport (eval.hpp:28-33) */
+typedef struct qvg_probe_report {
+    double overlap_at_k;
+    uint64_t sample_size;
+    uint32_t k;
+    uint32_t go; /* overlap_at_k > 0.5 */
+} qvg_probe_report;
+
+/* qivr::compatibility_probe (eval.hpp:35-37, eval.cpp:196-222): the first
+ * min(sample_size, n) rows; the first min(1000, sample) of them as queries
+ * against the sample with exclude_identity; overlap = recall_at_k(code
+ * ranking, float ranking, k).  Errors as the reference (sample < 100,
+ * all-identical sample). */
+qvg_status qvg_compatibility_probe(int device, const float* data, uint64_t n, uint32_t dim,
+                                   uint64_t sample_size, uint32_t k, int scorer,
+                                   qvg_probe_report* out);
+
+/* qivr::EncodingDiagnostics (encoding.hpp) */
+typedef struct qvg_encoding_diagnostics {
+    uint64_t sample_size;
+    double p_s; /* strong bits / (rows * dim) */
+    double nu2; /* (1 + 3 p_s)^2 */
+} qvg_encoding_diagnostics;
+
+/* qivr::strong_bit_rate: index != NULL -> the index's signatures
+ * (encoding.cpp:150-167, data ignored); else raw-encoded data rows
+ * (encoding.cpp:132-148) on `device`. */
+qvg_status qvg_strong_bit_rate(qvg_index* index, const float* data, uint64_t count, uint32_t dim,
+                               int device, qvg_encoding_diagnostics* out);
 
 #ifdef __cplusplus
 }

@@ -189,6 +189,15 @@ class RefIndex:
         p = _ref_lib().qref_cold(self._h)
         return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (self.n, self.dim)).copy()
 
+    def strong_bit_rate(self):
+        """qivr::strong_bit_rate(index.signatures) (encoding.cpp:150-167)."""
+        L = _ref_lib()
+        L.qref_strong_bit_rate_index.argtypes = [C.c_void_p, C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        ps, nu2, n = C.c_double(), C.c_double(), C.c_uint64()
+        _ref_check(L.qref_strong_bit_rate_index(self._h, C.byref(ps), C.byref(nu2), C.byref(n)))
+        return dict(sample_size=n.value, p_s=ps.value, nu2=nu2.value)
+
     def cold_access_count(self):
         return _ref_lib().qref_cold_access_count(self._h)
 
@@ -271,6 +280,52 @@ def ref_brute_force_topk(base, queries, k, threads=None, scorer=0):
                                                 base.shape[1], k,
                                                 threads or os.cpu_count() or 1, scorer, out))
     return out
+
+
+REF_SCORERS = {"float_cosine": 0, "sm2": 1, "sign1": 2, "sq2": 3}
+
+
+def ref_brute_force_topk_ex(base, queries, k, scorer="float_cosine", exclude_identity=False,
+                            threads=None):
+    """qivr::brute_force_topk with any scorer and exclude_identity."""
+    L = _ref_lib()
+    if not hasattr(L.qref_brute_force_topk_ex, "_set"):
+        L.qref_brute_force_topk_ex.argtypes = [_f32p, C.c_uint64, _f32p, C.c_uint64, C.c_uint32,
+                                               C.c_uint32, C.c_uint32, C.c_int, C.c_int, _u32p]
+        L.qref_brute_force_topk_ex._set = True
+    base = np.ascontiguousarray(base, np.float32)
+    queries = np.ascontiguousarray(queries, np.float32).reshape(-1, base.shape[1])
+    out = np.empty((queries.shape[0], k), np.uint32)
+    _ref_check(L.qref_brute_force_topk_ex(base, base.shape[0], queries, queries.shape[0],
+                                          base.shape[1], k, threads or os.cpu_count() or 1,
+                                          REF_SCORERS[scorer], int(exclude_identity), out))
+    return out
+
+
+def ref_compatibility_probe(data, sample_size=10000, k=10, scorer="sm2"):
+    """qivr::compatibility_probe -> dict(overlap_at_k, sample_size, k, go)."""
+    L = _ref_lib()
+    L.qref_compatibility_probe.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32,
+                                           C.c_int, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
+    data = np.ascontiguousarray(data, np.float32)
+    ov, sn, go = C.c_double(), C.c_uint64(), C.c_int()
+    _ref_check(L.qref_compatibility_probe(data, data.shape[0], data.shape[1], sample_size, k,
+                                          REF_SCORERS[scorer], C.byref(ov), C.byref(sn),
+                                          C.byref(go)))
+    return dict(overlap_at_k=ov.value, sample_size=sn.value, k=k, go=bool(go.value))
+
+
+def ref_strong_bit_rate(data):
+    """qivr::strong_bit_rate(data, count, dim) -> dict(sample_size, p_s, nu2)."""
+    L = _ref_lib()
+    L.qref_strong_bit_rate_data.argtypes = [_f32p, C.c_uint64, C.c_uint32,
+                                            C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    data = np.ascontiguousarray(data, np.float32)
+    ps, nu2 = C.c_double(), C.c_double()
+    _ref_check(L.qref_strong_bit_rate_data(data, data.shape[0], data.shape[1], C.byref(ps),
+                                           C.byref(nu2)))
+    return dict(sample_size=data.shape[0], p_s=ps.value, nu2=nu2.value)
 
 
 # --------------------------------------------------------------------------

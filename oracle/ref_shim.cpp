@@ -192,6 +192,54 @@ int qref_beam_search(void* h, const uint64_t* qcode, uint32_t ef, uint32_t entry
 }
 
 // Exact top-k by brute force. scorer: 0 float_cosine, 1 sm2.
+// scorer 0..3 = float_cosine, sm2, sign1, sq2; rows shorter than k padded
+// with UINT32_MAX
+int qref_brute_force_topk_ex(const float* base, uint64_t n, const float* queries, uint64_t nq,
+                             uint32_t dim, uint32_t k, uint32_t threads, int scorer,
+                             int exclude_identity, uint32_t* out) {
+    return guarded([&] {
+        static const qivr::Scorer sc[4] = {qivr::Scorer::float_cosine, qivr::Scorer::sm2,
+                                           qivr::Scorer::sign1, qivr::Scorer::sq2};
+        auto res = qivr::brute_force_topk(base, n, queries, nq, dim, k, sc[scorer & 3], threads,
+                                          exclude_identity != 0);
+        for (uint64_t i = 0; i < nq; ++i)
+            for (uint32_t j = 0; j < k; ++j)
+                out[i * k + j] = j < res[i].size() ? res[i][j] : UINT32_MAX;
+    });
+}
+
+int qref_compatibility_probe(const float* data, uint64_t n, uint32_t dim, uint64_t sample_size,
+                             uint32_t k, int scorer, double* overlap, uint64_t* sample_n,
+                             int* go) {
+    return guarded([&] {
+        static const qivr::Scorer sc[4] = {qivr::Scorer::float_cosine, qivr::Scorer::sm2,
+                                           qivr::Scorer::sign1, qivr::Scorer::sq2};
+        const auto r = qivr::compatibility_probe(data, n, dim, sample_size, k, sc[scorer & 3]);
+        *overlap = r.overlap_at_k;
+        *sample_n = r.sample_size;
+        *go = r.go ? 1 : 0;
+    });
+}
+
+// strong_bit_rate(data) (encoding.cpp:132-148) and (store) (encoding.cpp:150-167)
+int qref_strong_bit_rate_data(const float* data, uint64_t count, uint32_t dim, double* p_s,
+                              double* nu2) {
+    return guarded([&] {
+        const auto d = qivr::strong_bit_rate(data, count, dim);
+        *p_s = d.p_s;
+        *nu2 = d.nu2;
+    });
+}
+
+int qref_strong_bit_rate_index(void* h, double* p_s, double* nu2, uint64_t* sample) {
+    return guarded([&] {
+        const auto d = qivr::strong_bit_rate(as_index(h)->signatures);
+        *p_s = d.p_s;
+        *nu2 = d.nu2;
+        *sample = d.sample_size;
+    });
+}
+
 int qref_brute_force_topk(const float* base, uint64_t n, const float* queries, uint64_t nq,
                           uint32_t dim, uint32_t k, uint32_t threads, int scorer,
                           uint32_t* out) {

@@ -29,6 +29,7 @@ __all__ = [
     "SearchParams", "SearchResult", "GpuIndex", "BuildParams", "query", "run_query_batch",
     "encode_queries", "QvgError", "InvalidArgument", "QvgRuntimeError", "CudaError",
     "OutOfMemory", "CapacityOverflow", "NotImplementedByQvg", "words_for_dim", "SENTINEL",
+    "brute_force_topk", "compatibility_probe", "strong_bit_rate", "SCORERS",
 ]
 
 N.lib()  # fail loudly at import when the CUDA library is missing
@@ -295,6 +296,57 @@ def encode_queries(x, device=0):
     _check(N.lib().qvg_encode(device, x.ctypes.data, nq, dim, qn.ctypes.data, codes.ctypes.data,
                               tau.ctypes.data, st.ctypes.data))
     return qn, codes, tau
+
+
+SCORERS = {"float_cosine": 0, "sm2": 1, "sign1": 2, "sq2": 3}
+
+
+def brute_force_topk(base, queries, k, scorer="float_cosine", exclude_identity=False,
+                     device=0, with_values=False):
+    """qivr::brute_force_topk (eval.cpp:81-168) on the GPU: exact top-k ids per
+    query (nq x k, short rows padded with SENTINEL).  with_values also returns
+    the float scores (float_cosine) or code distances, and the row counts."""
+    base = _f32(base)
+    q = _f32(queries, base.shape[1])
+    nq, dim = q.shape
+    ids = np.empty((nq, k), np.uint32)
+    cnt = np.empty(nq, np.uint32)
+    sc = np.empty((nq, k), np.float32)
+    ds = np.empty((nq, k), np.uint32)
+    s = SCORERS[scorer]
+    _check(N.lib().qvg_brute_force_topk(device, N.ptr(base), base.shape[0], N.ptr(q),
+                                        nq, dim, k, s, int(exclude_identity), ids.ctypes.data,
+                                        sc.ctypes.data if s == 0 else None,
+                                        ds.ctypes.data if s != 0 else None, cnt.ctypes.data))
+    if with_values:
+        return ids, (sc if s == 0 else ds), cnt
+    return ids
+
+
+def compatibility_probe(data, sample_size=10000, k=10, scorer="sm2", device=0):
+    """qivr::compatibility_probe (eval.cpp:196-222) -> dict(overlap_at_k,
+    sample_size, k, go)."""
+    data = _f32(data)
+    rep = N.qvg_probe_report()
+    _check(N.lib().qvg_compatibility_probe(device, N.ptr(data), data.shape[0],
+                                           data.shape[1], sample_size, k, SCORERS[scorer],
+                                           C.byref(rep)))
+    return dict(overlap_at_k=rep.overlap_at_k, sample_size=rep.sample_size, k=rep.k,
+                go=bool(rep.go))
+
+
+def strong_bit_rate(data=None, index: Optional["GpuIndex"] = None, device=0):
+    """qivr::strong_bit_rate of raw data rows (encoding.cpp:132-148) or of an
+    index's signatures (encoding.cpp:150-167) -> dict(sample_size, p_s, nu2)."""
+    d = N.qvg_encoding_diagnostics()
+    if index is not None:
+        _check(N.lib().qvg_strong_bit_rate(index._h, None, 0, 0, device, C.byref(d)))
+    else:
+        x = _f32(data) if data is not None else np.empty((0, 0), np.float32)
+        _check(N.lib().qvg_strong_bit_rate(None, N.ptr(x) if x.shape[0] else None,
+                                           x.shape[0], x.shape[1] if x.ndim == 2 else 0,
+                                           device, C.byref(d)))
+    return dict(sample_size=d.sample_size, p_s=d.p_s, nu2=d.nu2)
 
 
 def run_query_batch(index: GpuIndex, queries, params: SearchParams, threads=None

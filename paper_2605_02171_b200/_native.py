@@ -28,7 +28,8 @@ EXPORTED_SYMBOLS = (
     "qvg_last_error", "qvg_abi_version", "qvg_index_create", "qvg_index_load",
     "qvg_index_save", "qvg_index_destroy", "qvg_index_info", "qvg_index_set_stream",
     "qvg_index_export", "qvg_search", "qvg_search_ex", "qvg_beam_search", "qvg_encode",
-    "qvg_sm2_distance", "qvg_build",
+    "qvg_sm2_distance", "qvg_build", "qvg_brute_force_topk", "qvg_compatibility_probe",
+    "qvg_strong_bit_rate",
 )
 
 
@@ -62,6 +63,15 @@ class qvg_build_stats(C.Structure):
     _fields_ = [("seconds", C.c_double), ("reprunes", C.c_uint64), ("batches", C.c_uint64),
                 ("mean_degree", C.c_double), ("min_degree", C.c_uint32),
                 ("max_degree", C.c_uint32)]
+
+
+class qvg_probe_report(C.Structure):
+    _fields_ = [("overlap_at_k", C.c_double), ("sample_size", C.c_uint64), ("k", C.c_uint32),
+                ("go", C.c_uint32)]
+
+
+class qvg_encoding_diagnostics(C.Structure):
+    _fields_ = [("sample_size", C.c_uint64), ("p_s", C.c_double), ("nu2", C.c_double)]
 
 
 _lib = None
@@ -98,6 +108,10 @@ def lib():
     L.qvg_sm2_distance.argtypes = [vp, vp, vp, u64, vp]
     L.qvg_build.argtypes = [vp, u64, u32, C.POINTER(qvg_build_params), i32, C.POINTER(vp),
                             C.POINTER(qvg_build_stats)]
+    L.qvg_brute_force_topk.argtypes = [i32, vp, u64, vp, u64, u32, u32, i32, i32, vp, vp, vp, vp]
+    L.qvg_compatibility_probe.argtypes = [i32, vp, u64, u32, u64, u32, i32,
+                                          C.POINTER(qvg_probe_report)]
+    L.qvg_strong_bit_rate.argtypes = [vp, vp, u64, u32, i32, C.POINTER(qvg_encoding_diagnostics)]
     for name in EXPORTED_SYMBOLS:
         f = getattr(L, name)
         if name not in ("qvg_last_error", "qvg_abi_version", "qvg_index_destroy"):

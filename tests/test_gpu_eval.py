@@ -1,0 +1,126 @@
+"""GPU evaluation support against the compiled
+reference: exact brute-force top-k (float_cosine / sm2 / sign1 scorers),
+compatibility probe and strong-bit rate.  Bar: identical ids (ties by id),
+bit-identical float scores and distances, identical probe / rate values."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")
+
+import paper_2605_02171_b200 as Q  # noqa: E402
+from paper_2605_02171_b200.datasets import mixture  # noqa: E402
+
+
+@ref_only
+@pytest.mark.parametrize("n,dim,nq,k", [(5000, 100, 64, 10), (20000, 384, 100, 100),
+                                        (3000, 65, 33, 7), (4000, 1536, 20, 10),
+                                        (700, 3, 9, 256)])
+def test_float_ground_truth_matches_reference(n, dim, nq, k):
+    base, q = mixture(n, dim, max(2, n // 100), 0.35, seed=n + dim, nq=nq)
+    ids, sc, cnt = Q.brute_force_topk(base, q, k, with_values=True)
+    ref = O.ref_brute_force_topk_ex(base, q, k)
+    assert np.array_equal(ids, ref)
+    assert (cnt == min(k, n)).all()
+    for i in range(0, nq, max(1, nq // 8)):  # scores are dot_f32, bit for bit
+        for j in range(0, min(k, n), max(1, k // 5)):
+            assert sc[i, j].view(np.uint32) == O.ref_dot(q[i], base[ids[i, j]]).view(np.uint32)
+
+
+def test_float_ground_truth_golden():
+    g = load_golden("g1")
+    assert np.array_equal(Q.brute_force_topk(g["cold"], g["queries"], 10), g["gt10"])
+
+
+@ref_only
+@pytest.mark.parametrize("scorer", ["sm2", "sign1"])
+@pytest.mark.parametrize("dim", [64, 100, 768])
+def test_code_scorers_match_reference(scorer, dim):
+    base, q = mixture(6000, dim, 40, 0.35, seed=dim, nq=50)
+    ids, d, cnt = Q.brute_force_topk(base, q, 20, scorer=scorer, with_values=True)
+    assert np.array_equal(ids, O.ref_brute_force_topk_ex(base, q, 20, scorer=scorer))
+    # distances: sm2 / hamming of the raw (unnormalised) codes
+    W = Q.words_for_dim(dim)
+    for i in (0, 7, 49):
+        qc, _ = O.ref_encode_raw(q[i])
+        for j in (0, 5, 19):
+            bc, _ = O.ref_encode_raw(base[ids[i, j]])
+            want = O.ref_sm2(qc, bc) if scorer == "sm2" else \
+                int(sum(bin(int(a) ^ int(b)).count("1") for a, b in zip(qc[:W], bc[:W])))
+            assert d[i, j] == want
+
+
+@ref_only
+@pytest.mark.parametrize("scorer", ["float_cosine", "sm2", "sign1"])
+def test_exclude_identity_and_ties(scorer):
+    base, _ = mixture(3000, 96, 20, 0.35, seed=5, nq=1)
+    base[100:110] = base[50]  # exact duplicates: equal scores, ranked by id
+    base[2000] = base[0]
+    q = base[:300]
+    for excl in (False, True):
+        got = Q.brute_force_topk(base, q, 15, scorer=scorer, exclude_identity=excl)
+        want = O.ref_brute_force_topk_ex(base, q, 15, scorer=scorer, exclude_identity=excl)
+        assert np.array_equal(got, want), (scorer, excl)
+
+
+def test_short_rows_padded():
+    base = np.random.default_rng(1).standard_normal((5, 16)).astype(np.float32)
+    ids, _, cnt = Q.brute_force_topk(base, base, 10, exclude_identity=True, with_values=True)
+    assert (cnt == 4).all()
+    assert (ids[:, 4:] == Q.SENTINEL).all()
+    assert all(i not in row[:4] for i, row in enumerate(ids))
+
+
+def test_device_buffers():
+    import torch
+    base, q = mixture(4000, 128, 40, 0.35, seed=9, nq=30)
+    a = Q.brute_force_topk(base, q, 10)
+    b = Q.brute_force_topk(torch.from_numpy(base).cuda(), torch.from_numpy(q).cuda(), 10)
+    assert np.array_equal(a, b)
+
+
+def test_errors():
+    x = np.ones((200, 8), np.float32)
+    with pytest.raises(Q.NotImplementedByQvg):
+        Q.brute_force_topk(x, x[:2], 5, scorer="sq2")
+    with pytest.raises(Q.NotImplementedByQvg):
+        Q.brute_force_topk(x, x[:2], 300)
+    x[3, 2] = np.inf
+    with pytest.raises(Q.InvalidArgument, match="non-finite coordinate"):
+        Q.brute_force_topk(x, x[:2], 5, scorer="sm2")
+
+
+@ref_only
+@pytest.mark.parametrize("scorer", ["sm2", "sign1"])
+def test_compatibility_probe_matches_reference(scorer):
+    for sigma_mode in ("literal", "norm"):
+        data, _ = mixture(5000, 128, 50, 0.35, seed=17, nq=1, sigma_mode=sigma_mode)
+        got = Q.compatibility_probe(data, sample_size=3000, k=10, scorer=scorer)
+        want = O.ref_compatibility_probe(data, sample_size=3000, k=10, scorer=scorer)
+        assert got["overlap_at_k"] == want["overlap_at_k"]
+        assert got["go"] == want["go"] and got["sample_size"] == want["sample_size"] == 3000
+
+
+def test_compatibility_probe_errors():
+    x = np.random.default_rng(0).standard_normal((99, 8)).astype(np.float32)
+    with pytest.raises(Q.InvalidArgument, match="sample too small"):
+        Q.compatibility_probe(x)
+    y = np.tile(x[:1], (150, 1))
+    with pytest.raises(Q.InvalidArgument, match="degenerate sample"):
+        Q.compatibility_probe(y)
+
+
+@ref_only
+def test_strong_bit_rate_matches_reference():
+    data, _ = mixture(3000, 100, 30, 0.35, seed=3, nq=1)
+    got = Q.strong_bit_rate(data)
+    want = O.ref_strong_bit_rate(data)
+    assert got == want
+    ref = O.RefIndex.build(data, m=8, ef_c=32, alpha=1.2, threads=4)
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    assert Q.strong_bit_rate(index=ix) == ref.strong_bit_rate()
+    with pytest.raises(Q.InvalidArgument, match="empty sample"):
+        Q.strong_bit_rate(np.empty((0, 4), np.float32))
