@@ -222,11 +222,11 @@ qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim, const qvg_buil
 #define QVG_SCORER_FLOAT_COSINE 0
 #define QVG_SCORER_SM2 1
 #define QVG_SCORER_SIGN1 2
-#define QVG_SCORER_SQ2 3 /* not implemented on the GPU (QVG_NOT_IMPLEMENTED) */
+#define QVG_SCORER_SQ2 3
 
 /* qivr::brute_force_topk (eval.hpp:19-21, eval.cpp:81-168): exact top-k of
  * every base row per query.  float_cosine ranks dot_f32 (the 4-chain double
- * dot) descending; sm2 / sign1 rank the raw codes' distances ascending; ties
+ * dot) descending; sm2 / sign1 / sq2 rank the raw codes' distances ascending; ties
  * by ascending id; exclude_identity skips row j == query index.  base n x dim,
  * queries nq x dim (host or device).  out_ids nq x k (rows shorter than k
  * padded with UINT32_MAX); out_scores (float_cosine) / out_dists (code
@@ -235,6 +235,14 @@ qvg_status qvg_brute_force_topk(int device, const float* base, uint64_t n, const
                                 uint64_t nq, uint32_t dim, uint32_t k, int scorer,
                                 int exclude_identity, uint32_t* out_ids, float* out_scores,
                                 uint32_t* out_dists, uint32_t* out_count);
+
+/* Raw (unnormalised) row encoders of the code scorers: sm2 = encode_sm2
+ * (encoding.cpp:32-58; out n x 2W u64, reference layout, out_tau n x f32
+ * nullable), sign1 = encode_sign1 (encoding.cpp:60-72; n x W u64), sq2 =
+ * encode_sq2 (encoding.cpp:74-106; n x dim u8).  Non-finite input ->
+ * QVG_INVALID_ARGUMENT "encode: non-finite coordinate". */
+qvg_status qvg_encode_rows(int device, const float* x, uint64_t n, uint32_t dim, int scorer,
+                           void* out_codes, float* out_tau);
 
 /* qivr::ProbeReport (eval.hpp:28-33) */
 typedef struct qvg_probe_report {

@@ -302,6 +302,26 @@ def ref_brute_force_topk_ex(base, queries, k, scorer="float_cosine", exclude_ide
     return out
 
 
+def ref_encode_sq2(x):
+    """qivr::encode_sq2 -> dim bytes."""
+    L = _ref_lib()
+    L.qref_encode_sq2.argtypes = [_f32p, C.c_uint32, C.c_void_p]
+    x = np.ascontiguousarray(x, np.float32).reshape(-1)
+    out = np.empty(x.size, np.uint8)
+    _ref_check(L.qref_encode_sq2(x, x.size, out.ctypes.data))
+    return out
+
+
+def ref_encode_sign1(x):
+    """qivr::encode_sign1 -> ceil(dim/64) words."""
+    L = _ref_lib()
+    L.qref_encode_sign1.argtypes = [_f32p, C.c_uint32, _u64p]
+    x = np.ascontiguousarray(x, np.float32).reshape(-1)
+    out = np.empty(words_for_dim(x.size), np.uint64)
+    _ref_check(L.qref_encode_sign1(x, x.size, out))
+    return out
+
+
 def ref_compatibility_probe(data, sample_size=10000, k=10, scorer="sm2"):
     """qivr::compatibility_probe -> dict(overlap_at_k, sample_size, k, go)."""
     L = _ref_lib()

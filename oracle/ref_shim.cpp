@@ -192,6 +192,22 @@ int qref_beam_search(void* h, const uint64_t* qcode, uint32_t ef, uint32_t entry
 }
 
 // Exact top-k by brute force. scorer: 0 float_cosine, 1 sm2.
+// qivr::encode_sq2 (encoding.cpp:74-106): dim bytes
+int qref_encode_sq2(const float* x, uint32_t dim, uint8_t* out) {
+    return guarded([&] {
+        const auto c = qivr::encode_sq2({x, dim});
+        std::memcpy(out, c.codes.data(), dim);
+    });
+}
+
+// qivr::encode_sign1 (encoding.cpp:60-72): ceil(dim/64) words
+int qref_encode_sign1(const float* x, uint32_t dim, uint64_t* out) {
+    return guarded([&] {
+        const auto c = qivr::encode_sign1({x, dim});
+        std::memcpy(out, c.bits.data(), c.bits.size() * 8);
+    });
+}
+
 // scorer 0..3 = float_cosine, sm2, sign1, sq2; rows shorter than k padded
 // with UINT32_MAX
 int qref_brute_force_topk_ex(const float* base, uint64_t n, const float* queries, uint64_t nq,

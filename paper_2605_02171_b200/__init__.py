@@ -29,7 +29,7 @@ __all__ = [
     "SearchParams", "SearchResult", "GpuIndex", "BuildParams", "query", "run_query_batch",
     "encode_queries", "QvgError", "InvalidArgument", "QvgRuntimeError", "CudaError",
     "OutOfMemory", "CapacityOverflow", "NotImplementedByQvg", "words_for_dim", "SENTINEL",
-    "brute_force_topk", "compatibility_probe", "strong_bit_rate", "SCORERS",
+    "brute_force_topk", "compatibility_probe", "strong_bit_rate", "SCORERS", "encode_rows",
 ]
 
 N.lib()  # fail loudly at import when the CUDA library is missing
@@ -321,6 +321,28 @@ def brute_force_topk(base, queries, k, scorer="float_cosine", exclude_identity=F
     if with_values:
         return ids, (sc if s == 0 else ds), cnt
     return ids
+
+
+def encode_rows(x, scorer="sm2", device=0):
+    """Raw row encoders (encode_sm2 / encode_sign1 / encode_sq2, encoding.cpp:
+    32-106): sm2 -> (codes[n,2W] u64, tau[n]); sign1 -> bits[n,W] u64;
+    sq2 -> codes[n,dim] u8."""
+    x = _f32(x)
+    if x.ndim == 1:
+        x = x.reshape(1, -1)
+    n, dim = x.shape
+    s = SCORERS[scorer]
+    W = words_for_dim(dim)
+    if s == 1:
+        out = np.empty((n, 2 * W), np.uint64)
+    elif s == 2:
+        out = np.empty((n, W), np.uint64)
+    else:
+        out = np.empty((n, dim), np.uint8)
+    tau = np.empty(n, np.float32)
+    _check(N.lib().qvg_encode_rows(device, N.ptr(x), n, dim, s, out.ctypes.data,
+                                   tau.ctypes.data if s == 1 else None))
+    return (out, tau) if s == 1 else out
 
 
 def compatibility_probe(data, sample_size=10000, k=10, scorer="sm2", device=0):

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "qvg_index_save", "qvg_index_destroy", "qvg_index_info", "qvg_index_set_stream",
     "qvg_index_export", "qvg_search", "qvg_search_ex", "qvg_beam_search", "qvg_encode",
     "qvg_sm2_distance", "qvg_build", "qvg_brute_force_topk", "qvg_compatibility_probe",
-    "qvg_strong_bit_rate",
+    "qvg_strong_bit_rate", "qvg_encode_rows",
 )
 
 
@@ -111,6 +111,7 @@ def lib():
     L.qvg_brute_force_topk.argtypes = [i32, vp, u64, vp, u64, u32, u32, i32, i32, vp, vp, vp, vp]
     L.qvg_compatibility_probe.argtypes = [i32, vp, u64, u32, u64, u32, i32,
                                           C.POINTER(qvg_probe_report)]
+    L.qvg_encode_rows.argtypes = [i32, vp, u64, u32, i32, vp, vp]
     L.qvg_strong_bit_rate.argtypes = [vp, vp, u64, u32, i32, C.POINTER(qvg_encoding_diagnostics)]
     for name in EXPORTED_SYMBOLS:
         f = getattr(L, name)

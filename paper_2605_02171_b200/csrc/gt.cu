@@ -12,6 +12,7 @@
 //   encode_sm2_into       encoding.cpp:32-45 raw (unnormalised) 2-bit code,
 //                                           tau = float(sum|x| / D) (:23-30)
 //   encode_sign1          encoding.cpp:60-72 sign bit == the sm2 pos bit
+//   encode_sq2            encoding.cpp:74-106, sq2_distance_bytes encoding.hpp:203-210
 //   compatibility_probe   eval.cpp:196-222
 //   strong_bit_rate       encoding.cpp:132-167
 //
@@ -26,9 +27,10 @@
 // shared memory); a tile's keys that beat the current k-th are appended and
 // the list re-sorted (warp bitonic sort), which is rare after the first
 // tiles.  Row ranges are split over gridDim.y and the per-split lists merged.
-// sm2 / sign1: the same selection over integer distances of raw codes.
+// sm2 / sign1 / sq2: the same selection over integer distances of raw codes.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -115,10 +117,12 @@ struct TopkArgs {
     const float* queries;  // float scorer: nq x dim
     const uint4* bcodes;   // code scorers: n x W chunks
     const uint4* qcodes;   // code scorers: nq x W chunks
+    const uint4* bsq;      // sq2: n x Dq bytes (zero padded)
+    const uint4* qsq;      // sq2: nq x Dq bytes
     uint64_t n, nq, rows_per_split;
-    uint32_t dim, W, k, S;
+    uint32_t dim, W, Dq, k, S;
     int exclude_identity;
-    int scorer;            // 0 float_cosine, 1 sm2, 2 sign1
+    int scorer;            // 0 float_cosine, 1 sm2, 2 sign1, 3 sq2
     uint64_t* part;        // nq x S x k keys
 };
 
@@ -141,11 +145,19 @@ __global__ void __launch_bounds__(256) topk_kernel(const TopkArgs a) {
     uint64_t* L = lists + (size_t)w * 2 * kMaxK;
     uint32_t ln = 0;
 
-    if (a.scorer != 0) {  // stage the block's query codes once
+    if (a.scorer == 1 || a.scorer == 2) {  // stage the block's query codes once
         uint4* qc = reinterpret_cast<uint4*>(stage);
         for (uint32_t i = tid; i < kQ * a.W; i += blockDim.x) {
             const uint32_t q = i / a.W, c = i % a.W;
             qc[i] = q0 + q < a.nq ? a.qcodes[(q0 + q) * a.W + c] : make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+    } else if (a.scorer == 3) {
+        uint4* qs = reinterpret_cast<uint4*>(stage);
+        const uint32_t V = a.Dq / 16;
+        for (uint32_t i = tid; i < kQ * V; i += blockDim.x) {
+            const uint32_t q = i / V, c = i % V;
+            qs[i] = q0 + q < a.nq ? a.qsq[(q0 + q) * V + c] : make_uint4(0, 0, 0, 0);
         }
         __syncthreads();
     }
@@ -229,6 +241,29 @@ __global__ void __launch_bounds__(256) topk_kernel(const TopkArgs a) {
                     __dadd_rn(__dadd_rn(acc[q][0], acc[q][1]), __dadd_rn(acc[q][2], acc[q][3])));
                 key[q] = score_key(s, (uint32_t)row);
             }
+        } else if (a.scorer == 3) {  // sq2_distance_bytes: sum |a_i - b_i|
+            const uint4* qs = reinterpret_cast<const uint4*>(stage);
+            const uint32_t V = a.Dq / 16;
+            uint32_t d[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) d[q] = 0;
+            if (rv) {
+                const uint4* rc = a.bsq + row * V;
+                for (uint32_t c = 0; c < V; ++c) {
+                    const uint4 v = __ldg(rc + c);
+#pragma unroll
+                    for (int q = 0; q < kQ; ++q) {
+                        const uint4 u = qs[q * V + c];
+                        uint32_t s = d[q];
+                        s = __dp4a(__vabsdiffu4(u.x, v.x), 0x01010101u, s);
+                        s = __dp4a(__vabsdiffu4(u.y, v.y), 0x01010101u, s);
+                        s = __dp4a(__vabsdiffu4(u.z, v.z), 0x01010101u, s);
+                        d[q] = __dp4a(__vabsdiffu4(u.w, v.w), 0x01010101u, s);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) key[q] = ((uint64_t)d[q] << 32) | (uint32_t)row;
         } else {
             const uint4* qc = reinterpret_cast<const uint4*>(stage);
             uint32_t d[kQ];
@@ -311,7 +346,8 @@ __global__ void merge_kernel(const uint64_t* __restrict__ part, uint64_t nq, uin
 __global__ void __launch_bounds__(256) encode_raw_kernel(const float* __restrict__ x,
                                                          uint64_t rows, uint32_t dim,
                                                          uint4* __restrict__ codes,
-                                                         uint32_t* __restrict__ bad) {
+                                                         uint32_t* __restrict__ bad,
+                                                         float* __restrict__ tau_out) {
     extern __shared__ __align__(16) float rbuf[];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t r = (uint64_t)blockIdx.x * 8 + wib;
@@ -349,6 +385,64 @@ __global__ void __launch_bounds__(256) encode_raw_kernel(const float* __restrict
             }
         }
         codes[r * W + wd] = make_uint4(p0, p1, s0, s1);
+    }
+    if (lane == 0 && !fin) atomicOr(bad, 1u);
+    if (lane == 0 && tau_out) tau_out[r] = tau;
+}
+
+// encode_sq2 (encoding.cpp:74-106): warp per row; lane 0 runs the two
+// index-ordered double reductions.  The reference's C++ build (gnu++20, -O3,
+// FMA-capable -march) contracts `var += (v - mean) * (v - mean)` into an FMA,
+// so the chain is fma(d, d, var).  Bucket b = int((v - lo) / width) in float
+// with x86 truncation semantics (out-of-range / NaN -> INT_MIN), clamped to
+// [0, 3]; a zero-spread row is all zeros.
+__global__ void __launch_bounds__(256) encode_sq2_kernel(const float* __restrict__ x,
+                                                         uint64_t rows, uint32_t dim,
+                                                         uint32_t Dq, uint8_t* __restrict__ codes,
+                                                         uint32_t* __restrict__ bad) {
+    extern __shared__ __align__(16) float sbuf[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t r = (uint64_t)blockIdx.x * 8 + wib;
+    if (r >= rows) return;
+    float* row = sbuf + (size_t)wib * dim;
+    const float* src = x + r * dim;
+    bool fin = true;
+    for (uint32_t i = lane; i < dim; i += 32) {
+        const float v = __ldg(src + i);
+        fin &= isfinite(v);
+        row[i] = v;
+    }
+    fin = __all_sync(kAll, fin);
+    __syncwarp();
+    float lo_l = 0.0f, width_l = 0.0f;
+    int ok_l = 0;
+    if (lane == 0 && fin) {
+        double mean = 0.0;
+        for (uint32_t i = 0; i < dim; ++i) mean = __dadd_rn(mean, (double)row[i]);
+        mean = __ddiv_rn(mean, (double)dim);
+        double var = 0.0;
+        for (uint32_t i = 0; i < dim; ++i) {
+            const double d = __dsub_rn((double)row[i], mean);
+            var = __fma_rn(d, d, var);
+        }
+        const double sd = __dsqrt_rn(__ddiv_rn(var, (double)dim));
+        if (sd > 0.0) {
+            ok_l = 1;
+            lo_l = __double2float_rn(__dsub_rn(mean, __dmul_rn(2.0, sd)));
+            width_l = __double2float_rn(sd);
+        }
+    }
+    const int ok = __shfl_sync(kAll, ok_l, 0);
+    const float lo = __shfl_sync(kAll, lo_l, 0), width = __shfl_sync(kAll, width_l, 0);
+    uint8_t* out = codes + r * Dq;
+    for (uint32_t i = lane; i < Dq; i += 32) {
+        int b = 0;
+        if (ok && i < dim) {
+            const float t = __fdiv_rn(__fsub_rn(row[i], lo), width);
+            b = (t >= -2147483648.0f && t < 2147483648.0f) ? (int)t : INT_MIN;
+            b = b < 0 ? 0 : (b > 3 ? 3 : b);
+        }
+        out[i] = (uint8_t)b;
     }
     if (lane == 0 && !fin) atomicOr(bad, 1u);
 }
@@ -403,17 +497,18 @@ qvg_status device_view(const float* src, size_t elems, DevBuf& buf, const float*
 }
 
 qvg_status encode_raw(const float* x, uint64_t rows, uint32_t dim, uint4* codes, uint32_t* d_bad,
-                      cudaStream_t s) {
+                      cudaStream_t s, float* tau = nullptr) {
     if (!rows) return QVG_OK;
     const size_t smem = 8ull * dim * 4;
     if (smem > 200 * 1024) {
-        set_error("brute_force_topk: dim too large for the code scorers");
+        set_error("encode: dim too large for the row encoders");
         return QVG_NOT_IMPLEMENTED;
     }
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(encode_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-    encode_raw_kernel<<<(unsigned)((rows + 7) / 8), 256, smem, s>>>(x, rows, dim, codes, d_bad);
+    encode_raw_kernel<<<(unsigned)((rows + 7) / 8), 256, smem, s>>>(x, rows, dim, codes, d_bad,
+                                                                      tau);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QVG_OK : cuda_status(e, "encode_raw");
 }
@@ -435,7 +530,35 @@ qvg_status topk_device(int device, const float* d_base, uint64_t n, const float*
     a.k = k;
     a.exclude_identity = exclude_identity;
     a.scorer = scorer;
-    if (scorer != 0) {
+    a.Dq = (dim + 15) & ~15u;
+    DevBuf bsq, qsq;
+    if (scorer == 3) {
+        const size_t esmem = 8ull * dim * 4;
+        if (esmem > 200 * 1024 || (size_t)kQ * a.Dq > 96 * 1024) {
+            set_error("brute_force_topk: dim too large for the sq2 scorer");
+            return QVG_NOT_IMPLEMENTED;
+        }
+        if (!bsq.alloc(n * (size_t)a.Dq) || !qsq.alloc(nq * (size_t)a.Dq) || !bad.alloc(4))
+            return cuda_status(cudaErrorMemoryAllocation, "brute_force_topk");
+        cudaMemsetAsync(bad.p, 0, 4, s);
+        if (esmem > 48 * 1024)
+            cudaFuncSetAttribute(encode_sq2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)esmem);
+        encode_sq2_kernel<<<(unsigned)((n + 7) / 8), 256, esmem, s>>>(
+            d_base, n, dim, a.Dq, static_cast<uint8_t*>(bsq.p), static_cast<uint32_t*>(bad.p));
+        encode_sq2_kernel<<<(unsigned)((nq + 7) / 8), 256, esmem, s>>>(
+            d_q, nq, dim, a.Dq, static_cast<uint8_t*>(qsq.p), static_cast<uint32_t*>(bad.p));
+        uint32_t hbad = 0;
+        cudaError_t e = cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_status(e, "encode_sq2");
+        if (hbad) {
+            set_error("encode: non-finite coordinate");
+            return QVG_INVALID_ARGUMENT;
+        }
+        a.bsq = static_cast<const uint4*>(bsq.p);
+        a.qsq = static_cast<const uint4*>(qsq.p);
+    } else if (scorer != 0) {
         if (!bcodes.alloc(n * W * 16ull) || !qcodes.alloc(nq * W * 16ull) || !bad.alloc(4))
             return cuda_status(cudaErrorMemoryAllocation, "brute_force_topk");
         cudaMemsetAsync(bad.p, 0, 4, s);
@@ -469,7 +592,9 @@ qvg_status topk_device(int device, const float* d_base, uint64_t n, const float*
     a.rows_per_split = ((n + S - 1) / S + kRowsT - 1) / kRowsT * kRowsT;
     if (!part.alloc(nq * S * k * 8ull)) return cuda_status(cudaErrorMemoryAllocation, "brute_force_topk");
     a.part = static_cast<uint64_t*>(part.p);
-    const size_t stage = scorer == 0 ? (size_t)kKC * (kRowsT + kQ) * 8 : (size_t)kQ * W * 16;
+    const size_t stage = scorer == 0   ? (size_t)kKC * (kRowsT + kQ) * 8
+                         : scorer == 3 ? (size_t)kQ * a.Dq
+                                       : (size_t)kQ * W * 16;
     const size_t smem = kListBytes + kTileBytes + stage;
     cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -530,10 +655,6 @@ qvg_status qvg_brute_force_topk(int device, const float* base, uint64_t n, const
         set_error("brute_force_topk: unknown scorer");
         return QVG_INVALID_ARGUMENT;
     }
-    if (scorer == 3) {
-        set_error("brute_force_topk: the sq2 scorer is not implemented on the GPU");
-        return QVG_NOT_IMPLEMENTED;
-    }
     if (k > kMaxK) {
         set_error("brute_force_topk: k > 256 is not supported");
         return QVG_NOT_IMPLEMENTED;
@@ -574,6 +695,73 @@ qvg_status qvg_brute_force_topk(int device, const float* base, uint64_t n, const
     if ((st = oi.back()) != QVG_OK || (st = os.back()) != QVG_OK || (st = od.back()) != QVG_OK ||
         (st = oc.back()) != QVG_OK)
         return st;
+    return QVG_OK;
+}
+
+qvg_status qvg_encode_rows(int device, const float* x, uint64_t n, uint32_t dim, int scorer,
+                           void* out_codes, float* out_tau) {
+    if (dim == 0) {
+        set_error("encode: empty vector");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (scorer < 1 || scorer > 3) {
+        set_error("encode_rows: scorer must be sm2, sign1 or sq2");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (n == 0) return QVG_OK;
+    if (!x || !out_codes) {
+        set_error("encode_rows: null buffer");
+        return QVG_INVALID_ARGUMENT;
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    qvg_status st;
+    DevBuf xb, tmp, bad;
+    const float* d = nullptr;
+    if ((st = device_view(x, n * (size_t)dim, xb, &d, nullptr)) != QVG_OK) return st;
+    if (!bad.alloc(4)) return cuda_status(cudaErrorMemoryAllocation, "encode_rows");
+    cudaMemset(bad.p, 0, 4);
+    const uint32_t W = (dim + 63) / 64;
+    const size_t out_bytes = scorer == 3 ? n * (size_t)dim : n * (size_t)W * 8 * (scorer == 1 ? 2 : 1);
+    OutBuf oc, ot;
+    if ((st = oc.bind(out_codes, out_bytes)) != QVG_OK) return st;
+    if ((st = ot.bind(scorer == 1 ? out_tau : nullptr, n * 4ull)) != QVG_OK) return st;
+    if (scorer == 3) {
+        const size_t esmem = 8ull * dim * 4;
+        if (esmem > 200 * 1024) {
+            set_error("encode: dim too large for the row encoders");
+            return QVG_NOT_IMPLEMENTED;
+        }
+        if (esmem > 48 * 1024)
+            cudaFuncSetAttribute(encode_sq2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)esmem);
+        encode_sq2_kernel<<<(unsigned)((n + 7) / 8), 256, esmem>>>(
+            d, n, dim, dim, static_cast<uint8_t*>(oc.dev), static_cast<uint32_t*>(bad.p));
+    } else {
+        DevBuf chunks, words;
+        if (!chunks.alloc(n * W * 16ull) || !words.alloc(n * W * 16ull))
+            return cuda_status(cudaErrorMemoryAllocation, "encode_rows");
+        if ((st = encode_raw(d, n, dim, static_cast<uint4*>(chunks.p), static_cast<uint32_t*>(bad.p),
+                             nullptr, static_cast<float*>(ot.dev))) != QVG_OK)
+            return st;
+        // reference layout per row: W pos words then W strong words; sign1
+        // keeps the pos words (the sign bit is the sm2 pos bit)
+        launch_chunks_to_codes(static_cast<const uint4*>(chunks.p), n, W,
+                               static_cast<uint64_t*>(words.p), nullptr);
+        if (scorer == 1)
+            e = cudaMemcpy(oc.dev, words.p, n * W * 16ull, cudaMemcpyDeviceToDevice);
+        else
+            e = cudaMemcpy2D(oc.dev, W * 8, words.p, W * 16, W * 8, n, cudaMemcpyDeviceToDevice);
+        if (e != cudaSuccess) return cuda_status(e, "encode_rows");
+    }
+    uint32_t hbad = 0;
+    if ((e = cudaMemcpy(&hbad, bad.p, 4, cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return cuda_status(e, "encode_rows");
+    if (hbad) {
+        set_error("encode: non-finite coordinate");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if ((st = oc.back()) != QVG_OK || (st = ot.back()) != QVG_OK) return st;
     return QVG_OK;
 }
 

@@ -36,12 +36,14 @@ def test_float_ground_truth_golden():
 
 
 @ref_only
-@pytest.mark.parametrize("scorer", ["sm2", "sign1"])
+@pytest.mark.parametrize("scorer", ["sm2", "sign1", "sq2"])
 @pytest.mark.parametrize("dim", [64, 100, 768])
 def test_code_scorers_match_reference(scorer, dim):
     base, q = mixture(6000, dim, 40, 0.35, seed=dim, nq=50)
     ids, d, cnt = Q.brute_force_topk(base, q, 20, scorer=scorer, with_values=True)
     assert np.array_equal(ids, O.ref_brute_force_topk_ex(base, q, 20, scorer=scorer))
+    if scorer == "sq2":  # sq2 codes are not exposed by the reference; ids pin them
+        return
     # distances: sm2 / hamming of the raw (unnormalised) codes
     W = Q.words_for_dim(dim)
     for i in (0, 7, 49):
@@ -54,7 +56,7 @@ def test_code_scorers_match_reference(scorer, dim):
 
 
 @ref_only
-@pytest.mark.parametrize("scorer", ["float_cosine", "sm2", "sign1"])
+@pytest.mark.parametrize("scorer", ["float_cosine", "sm2", "sign1", "sq2"])
 def test_exclude_identity_and_ties(scorer):
     base, _ = mixture(3000, 96, 20, 0.35, seed=5, nq=1)
     base[100:110] = base[50]  # exact duplicates: equal scores, ranked by id
@@ -85,16 +87,15 @@ def test_device_buffers():
 def test_errors():
     x = np.ones((200, 8), np.float32)
     with pytest.raises(Q.NotImplementedByQvg):
-        Q.brute_force_topk(x, x[:2], 5, scorer="sq2")
-    with pytest.raises(Q.NotImplementedByQvg):
         Q.brute_force_topk(x, x[:2], 300)
     x[3, 2] = np.inf
-    with pytest.raises(Q.InvalidArgument, match="non-finite coordinate"):
-        Q.brute_force_topk(x, x[:2], 5, scorer="sm2")
+    for scorer in ("sm2", "sq2"):
+        with pytest.raises(Q.InvalidArgument, match="non-finite coordinate"):
+            Q.brute_force_topk(x, x[:2], 5, scorer=scorer)
 
 
 @ref_only
-@pytest.mark.parametrize("scorer", ["sm2", "sign1"])
+@pytest.mark.parametrize("scorer", ["sm2", "sign1", "sq2"])
 def test_compatibility_probe_matches_reference(scorer):
     for sigma_mode in ("literal", "norm"):
         data, _ = mixture(5000, 128, 50, 0.35, seed=17, nq=1, sigma_mode=sigma_mode)
@@ -124,3 +125,45 @@ def test_strong_bit_rate_matches_reference():
     assert Q.strong_bit_rate(index=ix) == ref.strong_bit_rate()
     with pytest.raises(Q.InvalidArgument, match="empty sample"):
         Q.strong_bit_rate(np.empty((0, 4), np.float32))
+
+
+@ref_only
+def test_sq2_edge_rows():
+    """sq2 encoder edge cases: zero-spread rows (all bucket 0), constant offsets,
+    a single outlier, tiny and huge magnitudes — ranking identical to the reference."""
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((2000, 48)).astype(np.float32)
+    base[0] = 1.5           # zero spread
+    base[1] = 0.0
+    base[2, :] = 0.01
+    base[2, 7] = 40.0       # one outlier sets the scale
+    base[3] *= 1e-20
+    base[4] *= 1e20
+    base[5:40] = np.round(base[5:40])  # many exact ties in value
+    q = np.concatenate([base[:20], rng.standard_normal((20, 48)).astype(np.float32)])
+    assert np.array_equal(Q.brute_force_topk(base, q, 30, scorer="sq2"),
+                          O.ref_brute_force_topk_ex(base, q, 30, scorer="sq2"))
+
+
+@ref_only
+@pytest.mark.parametrize("dim", [1, 3, 48, 64, 100, 768, 1536])
+def test_row_encoders_bit_exact(dim):
+    """encode_sm2 / encode_sign1 / encode_sq2 on raw rows, byte for byte, including
+    zero-spread, outlier, tiny/huge and exactly-tied rows."""
+    rng = np.random.default_rng(dim)
+    x = rng.standard_normal((300, dim)).astype(np.float32)
+    x[0] = 1.5
+    x[1] = 0.0
+    x[2] *= 1e-30
+    x[3] *= 1e30
+    x[4] = np.round(x[4])
+    x[5, 0] = 1e4
+    codes, tau = Q.encode_rows(x, "sm2")
+    bits = Q.encode_rows(x, "sign1")
+    sq = Q.encode_rows(x, "sq2")
+    for i in range(x.shape[0]):
+        c, t = O.ref_encode_raw(x[i])
+        assert np.array_equal(codes[i], c), i
+        assert np.float32(tau[i]).view(np.uint32) == np.float32(t).view(np.uint32), i
+        assert np.array_equal(bits[i], O.ref_encode_sign1(x[i])), i
+        assert np.array_equal(sq[i], O.ref_encode_sq2(x[i])), i
