@@ -62,6 +62,14 @@ __device__ __forceinline__ uint32_t vhash(uint32_t id, uint32_t lg) {
 
 using namespace dev;  // sm2_chunk, TMA / mbarrier wrappers (bq_device.cuh)
 
+// per-phase cycle counters of the search loop: only in the instrumented build
+// (python paper_2605_02171_b200/build.py --variant phases -DQVG_PHASES)
+#ifdef QVG_PHASES
+#define QVG_PH(...) __VA_ARGS__
+#else
+#define QVG_PH(...)
+#endif
+
 // column 0 (code rows are one TMA box wide)
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint32_t r0,
                                             uint32_t r1, uint32_t r2, uint32_t r3,
@@ -72,6 +80,37 @@ __device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* ma
                                                 uint32_t r0, uint32_t r1, uint32_t r2,
                                                 uint32_t r3, uint64_t* bar) {
     dev::tma_gather4(dst, map, col, r0, r1, r2, r3, bar);
+}
+
+// SM2 distance of one staged row, taken by one of the LPR lanes that share
+// the row: part p (t = p, p+LPR, ... < W) reads chunk (rot + t - p) mod W,
+// rot = lane mod W — the per-lane rotation that keeps the 8 lanes of an
+// LDS.128 phase on distinct bank quads.  One lockstep loop (a per-lane wrap
+// point must not become a branch: divergent segments cost +50 %), unrolled by
+// 4 with the four chunk indices computed first so the eight loads can issue
+// together.
+__device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
+                                            const uint4* __restrict__ row, uint32_t W,
+                                            uint32_t rot, uint32_t part, uint32_t LPR) {
+    uint32_t d = 0;
+    const uint32_t iters = (W - part + LPR - 1) / LPR;
+    uint32_t cc = rot, i = 0;
+    auto nxt = [&](uint32_t x) {
+        x += LPR;
+        return x >= W ? x - W : x;
+    };
+    for (; i + 4 <= iters; i += 4) {
+        const uint32_t c0 = cc, c1 = nxt(c0), c2 = nxt(c1), c3 = nxt(c2);
+        cc = nxt(c3);
+        const uint4 q0 = qc[c0], v0 = row[c0], q1 = qc[c1], v1 = row[c1];
+        const uint4 q2 = qc[c2], v2 = row[c2], q3 = qc[c3], v3 = row[c3];
+        d += (sm2_chunk(q0, v0) + sm2_chunk(q1, v1)) + (sm2_chunk(q2, v2) + sm2_chunk(q3, v3));
+    }
+    for (; i < iters; ++i) {
+        d += sm2_chunk(qc[cc], row[cc]);
+        cc = nxt(cc);
+    }
+    return d;
 }
 
 // first index i in [0, n) with ordk(a[i]) >= x
@@ -432,7 +471,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         uint32_t spec_v[RW];
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
+        QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0;)
         for (;;) {
+            QVG_PH(long long tp0 = clock64();)
             c_eval += n;
             // (a) TMA-gather the code rows (double-buffered halves of SR rows)
             const uint32_t nsub = (n + SR - 1) / SR;
@@ -475,6 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     }
                 }
             }
+            QVG_PH(long long tp1 = clock64(); ph_issue += tp1 - tp0;)
             // (b) SM2 distances lane-per-row from the stage; contenders -> ctd/crp
             const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
             const uint64_t worst_a = (XA && na == xa) ? pa[xa - 1] : kInfKey;
@@ -562,6 +604,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             }
             for (uint32_t k = 0; !paired && k < nsub; ++k) {
                 const uint32_t h = k & 1u;
+                QVG_PH(long long tw0 = clock64();)
                 if (h == 0) {
                     mbar_wait(&bars[0], phase0);
                     phase0 ^= 1u;
@@ -569,6 +612,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     mbar_wait(&bars[1], phase1);
                     phase1 ^= 1u;
                 }
+                QVG_PH(ph_wait += clock64() - tw0;)
                 const uint32_t r0 = k * SR;
                 const uint32_t cnt = min(n - r0, SR);
                 const uint4* st = reinterpret_cast<const uint4*>(stage0 + h * stage_delta);
@@ -582,6 +626,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     uint32_t d = 0;
                     if (valid) {
                         const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
+                        // (row_sm2 here measured 0.8 % slower at W = 12)
                         uint32_t cc = rot;
 #pragma unroll 4
                         for (uint32_t c = 0; c < W; ++c) {
@@ -598,13 +643,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     uint32_t d = 0;
                     if (valid) {
                         const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
-                        uint32_t cc = rot;
-#pragma unroll 4
-                        for (uint32_t t = part; t < W; t += LPR) {
-                            d += sm2_chunk(qc[cc], rowp[cc]);
-                            cc += LPR;
-                            if (cc >= W) cc -= W;
-                        }
+                        d = row_sm2(qc, rowp, W, rot, part, LPR);
                     }
                     for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
                     const bool lead = valid && part == 0;
@@ -613,6 +652,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), h);
             }
             __syncwarp();
+            QVG_PH(long long tp2 = clock64(); ph_dist += tp2 - tp1;)
             // (L2 prefetch of the predicted next pick's neighbour rows here was
             // measured: TMA bulk prefetch +25% time, LSU line prefetch +0.7%)
 
@@ -753,6 +793,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 }
             }
 
+            QVG_PH(long long tp3 = clock64(); ph_merge += tp3 - tp2;)
             // (f) pick: first unexpanded pool entry at or after the hint, else
             // the top of the tie stack (every live tie entry has dist ==
             // worst(P).dist, so the reference's stop test, search.cpp:48, does
@@ -841,6 +882,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             for (int j = 0; j < RW; ++j)
                 if (keep[j]) cid[pos++] = v[j];
             __syncwarp();
+            QVG_PH(ph_pick += clock64() - tp3;)
         }
 
         // ---- outputs ------------------------------------------------------------
@@ -869,6 +911,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 c[7] = (uint32_t)qstatus;
             }
         }
+        QVG_PH(if (lane == 0 && a.qctr) {
+            uint32_t* c = a.qctr + q * 8;  // phases build only: cycles >> 4
+            c[3] = (uint32_t)(ph_issue >> 4);
+            c[4] = (uint32_t)(ph_wait >> 4);
+            c[5] = (uint32_t)((ph_dist - ph_wait) >> 4);
+            c[6] = (uint32_t)(ph_merge >> 4);
+            c[7] = (uint32_t)(ph_pick >> 4);
+        })
         if (a.do_rerank) {
             // rerank the NR best scored keys pk[0, NR) (P, then A when XA)
             const uint32_t NR = min(np + na, a.depth);

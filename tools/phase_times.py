@@ -7,15 +7,23 @@ os.environ["QVG_VARIANT"] = str(16 | int(os.environ.get("EXTRA_VARIANT", "0")))
 import paper_2605_02171_b200 as Q
 from paper_2605_02171_b200 import datasets, graphs
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
-vs = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+vs = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+nq = int(sys.argv[3]) if len(sys.argv) > 3 else 10000
 base, queries = datasets.config_data(cfg, nq=10000)
+queries = queries[:nq]
 g = graphs.load_graph(cfg, "literal", base.shape[0], base)
 qn, codes, _ = Q.encode_queries(base)
 ix = Q.GpuIndex.from_arrays(codes, g["adj"], qn, int(g["entry"]))
 for it in range(3):
     r = ix.search_ex(queries, k=10, ef=64, visited_slots=vs, pools=False)
 c = r["counters"].astype(np.float64) * 16
-print("kernel ms", r["stats"]["search_ms"])
-for i, name in enumerate(["search", "rerank_dots", "rank_out"]):
+st = r["stats"]
+print(f"nq {nq}: kernel ms {st['search_ms']:.4f} encode ms {st['encode_ms']:.4f} "
+      f"device ms {st['device_ms']:.4f} total ms {st['total_ms']:.4f} "
+      f"expansions/q {st['expansions'] / nq:.1f}")
+names = ["search", "rerank_dots", "rank_out"]
+if os.environ.get("QVG_LIB", "").endswith("phases/libqvg.so"):  # instrumented build
+    names += ["  issue+spec", "  tma_wait", "  distances", "  merge+tie", "  pick+adj+vis"]
+for i, name in enumerate(names):
     v = c[:, i]
     print(f"{name:12s} mean {v.mean()/1.9e3:8.1f} us  p50 {np.median(v)/1.9e3:8.1f}  p99 {np.percentile(v,99)/1.9e3:8.1f}  max {v.max()/1.9e3:8.1f}")
