@@ -82,6 +82,39 @@ __device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* ma
     dev::tma_gather4(dst, map, col, r0, r1, r2, r3, bar);
 }
 
+// Row distance accumulator in bit planes (Harley-Seal carry-save adders).
+// Per chunk the SM2 terms are four weight-1 words (x0, x1, o0, o1) and two
+// weight-2 words (a0, a1) (encoding.hpp:169-176: popc(x) + popc(x & (sa|sb)) +
+// 2 popc(x & sa & sb)).  Adding them through CSAs (LOP3s on the ALU pipe)
+// leaves one POPC per chunk instead of six: POPC runs on the XU pipe at a
+// quarter of the ALU rate on B200 (tools/popc_bench.cu: 0.5 vs 2 warp-ops per
+// SM per cycle), and the XU pipe was the busiest in the search kernel.
+__device__ __forceinline__ void csa(uint32_t& a, uint32_t b, uint32_t c, uint32_t& carry) {
+    const uint32_t u = a ^ b;
+    carry = (a & b) | (u & c);
+    a = u ^ c;
+}
+struct Sm2Acc {
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, d16 = 0;
+    __device__ __forceinline__ void add(const uint4 q, const uint4 v) {
+        const uint32_t x0 = q.x ^ v.x, x1 = q.y ^ v.y;
+        const uint32_t o0 = x0 & (q.z | v.z), o1 = x1 & (q.w | v.w);
+        const uint32_t a0 = x0 & q.z & v.z, a1 = x1 & q.w & v.w;
+        uint32_t c1, c2, f1, f2, e;
+        csa(ones, x0, x1, c1);   // weight 1 -> carries of weight 2
+        csa(ones, o0, o1, c2);
+        csa(twos, c1, c2, f1);   // weight 2 -> carries of weight 4
+        csa(twos, a0, a1, f2);
+        csa(fours, f1, f2, e);   // weight 4 -> carry of weight 8
+        d16 += __popc(eights & e);  // half adder at weight 8, carry counted
+        eights ^= e;
+    }
+    __device__ __forceinline__ uint32_t total() const {
+        return __popc(ones) + 2u * __popc(twos) + 4u * __popc(fours) + 8u * __popc(eights) +
+               16u * d16;
+    }
+};
+
 // SM2 distance of one staged row, taken by one of the LPR lanes that share
 // the row: part p (t = p, p+LPR, ... < W) reads chunk (rot + t - p) mod W,
 // rot = lane mod W — the per-lane rotation that keeps the 8 lanes of an
@@ -92,7 +125,7 @@ __device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* ma
 __device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
                                             const uint4* __restrict__ row, uint32_t W,
                                             uint32_t rot, uint32_t part, uint32_t LPR) {
-    uint32_t d = 0;
+    Sm2Acc acc;
     const uint32_t iters = (W - part + LPR - 1) / LPR;
     uint32_t cc = rot, i = 0;
     auto nxt = [&](uint32_t x) {
@@ -104,13 +137,16 @@ __device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
         cc = nxt(c3);
         const uint4 q0 = qc[c0], v0 = row[c0], q1 = qc[c1], v1 = row[c1];
         const uint4 q2 = qc[c2], v2 = row[c2], q3 = qc[c3], v3 = row[c3];
-        d += (sm2_chunk(q0, v0) + sm2_chunk(q1, v1)) + (sm2_chunk(q2, v2) + sm2_chunk(q3, v3));
+        acc.add(q0, v0);
+        acc.add(q1, v1);
+        acc.add(q2, v2);
+        acc.add(q3, v3);
     }
     for (; i < iters; ++i) {
-        d += sm2_chunk(qc[cc], row[cc]);
+        acc.add(qc[cc], row[cc]);
         cc = nxt(cc);
     }
-    return d;
+    return acc.total();
 }
 
 // first index i in [0, n) with ordk(a[i]) >= x
@@ -471,7 +507,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         uint32_t spec_v[RW];
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
-        QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0;)
+        QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0, ph_tma = 0;)
         for (;;) {
             QVG_PH(long long tp0 = clock64();)
             c_eval += n;
@@ -479,6 +515,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             const uint32_t nsub = (n + SR - 1) / SR;
             if (nsub > 0) issue(0, min(n, SR), 0);
             if (nsub > 1) issue(SR, min(n - SR, SR), 1);
+            QVG_PH(ph_tma += clock64() - tp0;)
             // speculative prefetch: adjacency row of the current best unexpanded
             // entry (the next pick unless this row inserts a better one)
             {
@@ -628,11 +665,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                         const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
                         // (row_sm2 here measured 0.8 % slower at W = 12)
                         uint32_t cc = rot;
+                        Sm2Acc acc;
 #pragma unroll 4
                         for (uint32_t c = 0; c < W; ++c) {
-                            d += sm2_chunk(qc[cc], rowp[cc]);
+                            acc.add(qc[cc], rowp[cc]);
                             cc = cc + 1u == W ? 0u : cc + 1u;
                         }
+                        d = acc.total();
                     }
                     emit(valid, d, valid ? cid[r0 + j] : kSentinel);
                 }
@@ -913,7 +952,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         }
         QVG_PH(if (lane == 0 && a.qctr) {
             uint32_t* c = a.qctr + q * 8;  // phases build only: cycles >> 4
-            c[3] = (uint32_t)(ph_issue >> 4);
+            c[2] = (uint32_t)(ph_tma >> 4);
+            c[3] = (uint32_t)((ph_issue - ph_tma) >> 4);
             c[4] = (uint32_t)(ph_wait >> 4);
             c[5] = (uint32_t)((ph_dist - ph_wait) >> 4);
             c[6] = (uint32_t)(ph_merge >> 4);
@@ -1046,8 +1086,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 a.out_scores[q * a.k + r] = __int_as_float(0x7fc00000);
             }
             if (lane == 0 && a.out_count) a.out_count[q] = NR < a.k ? NR : a.k;
+#ifndef QVG_PHASES  // slot 2 carries the TMA-issue time in the phases build
             if ((a.variant & 16u) && lane == 0 && a.qctr)
                 a.qctr[q * 8 + 2] = (uint32_t)((clock64() - t_dots) >> 4);
+#endif
         }
         __syncwarp();
     }

@@ -23,7 +23,8 @@ print(f"nq {nq}: kernel ms {st['search_ms']:.4f} encode ms {st['encode_ms']:.4f}
       f"expansions/q {st['expansions'] / nq:.1f}")
 names = ["search", "rerank_dots", "rank_out"]
 if os.environ.get("QVG_LIB", "").endswith("phases/libqvg.so"):  # instrumented build
-    names += ["  issue+spec", "  tma_wait", "  distances", "  merge+tie", "  pick+adj+vis"]
+    names[2] = "  tma_issue"
+    names += ["  spec_adj", "  tma_wait", "  distances", "  merge+tie", "  pick+adj+vis"]
 for i, name in enumerate(names):
     v = c[:, i]
     print(f"{name:12s} mean {v.mean()/1.9e3:8.1f} us  p50 {np.median(v)/1.9e3:8.1f}  p99 {np.percentile(v,99)/1.9e3:8.1f}  max {v.max()/1.9e3:8.1f}")
