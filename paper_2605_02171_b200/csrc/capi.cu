@@ -97,6 +97,31 @@ struct Mode {
     bool rerank;
 };
 
+__global__ void set_word_kernel(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+void launch_set_word(uint32_t* p, uint32_t v, cudaStream_t s) { set_word_kernel<<<1, 1, 0, s>>>(p, v); }
+
+// copy stream, its event and `chunks` pinned ready slots for the pipelined upload
+qvg_status ensure_copy_stream(qvg_index* h, uint64_t chunks) {
+    cudaError_t e;
+    if (!h->copy_stream) {
+        if ((e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_status(e, "cudaStreamCreate(copy)");
+        if ((e = cudaEventCreateWithFlags(&h->ev_copy, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_status(e, "cudaEventCreate(copy)");
+    }
+    if (h->ready_cap < chunks) {
+        if (h->ready_host) cudaFreeHost(h->ready_host);
+        h->ready_host = nullptr;
+        h->ready_cap = 0;
+        if ((e = cudaMallocHost(&h->ready_host, chunks * 4)) != cudaSuccess)
+            return cuda_status(e, "cudaMallocHost(ready)");
+        h->ready_cap = chunks;
+    }
+    return QVG_OK;
+}
+
 qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint64_t nq,
                uint32_t k, uint32_t ef, const qvg_search_opts* opts, Mode mode,
                uint32_t* out_ids, float* out_scores, uint32_t* out_count,
@@ -248,28 +273,44 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
 
     // ---- pipeline -------------------------------------------------------------
     uint32_t* d_flags = reinterpret_cast<uint32_t*>(static_cast<char*>(h->s_counter.p) + 32);
+    uint32_t* d_ready = reinterpret_cast<uint32_t*>(static_cast<char*>(h->s_counter.p) + 48);
     a.flags = d_flags;
-    cudaEventRecord(h->ev[0], s);
-    const void* din = user_in;
-    if (!in_dev) {
-        e = cudaMemcpyAsync(h->s_in.p, user_in, in_bytes, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return cuda_status(e, "H2D(queries)");
-        din = h->s_in.p;
-    }
-    cudaMemsetAsync(h->s_counter.p, 0, 64, s);  // work counter + flag word
-    cudaEventRecord(h->ev[1], s);
     // opt-in: the lane-0 FP64 chains stall the search warp; measured 3.10 ms
     // fused vs 3.02 ms with the separate encode kernel (cfg2, 10k queries)
     static const bool fused_env = [] {
         const char* v = getenv("QVG_FUSED");
         return v && v[0] == '1';
     }();
-    const bool fused = mode.encode && fused_env && 4ull * ix.dim <= search_stage_bytes(ix);
+    // Host queries: pipelined upload (QVG_PIPELINE=0 disables).  One search
+    // launch with the fused encode prologue starts first; a copy stream lands
+    // the queries chunk by chunk and publishes how many have landed; each
+    // warp waits for its query's chunk.  The upload hides under the search
+    // (no per-chunk launch tails), also for pageable buffers, since the
+    // kernel is already running while the driver stages them.
+    static const bool pipe_env = [] {
+        const char* v = getenv("QVG_PIPELINE");
+        return !(v && v[0] == '0');
+    }();
+    constexpr uint64_t kChunk = 1024;
+    const bool stage_ok = 4ull * ix.dim <= search_stage_bytes(ix);
+    const bool pipelined = mode.encode && !in_dev && pipe_env && stage_ok && nq >= 2 * kChunk;
+    cudaEventRecord(h->ev[0], s);
+    const void* din = user_in;
+    if (!in_dev && !pipelined) {
+        e = cudaMemcpyAsync(h->s_in.p, user_in, in_bytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_status(e, "H2D(queries)");
+    }
+    if (!in_dev) din = h->s_in.p;
+    cudaMemsetAsync(h->s_counter.p, 0, 64, s);  // work counter + flag word + ready count
+    cudaEventRecord(h->ev[1], s);
+    const bool fused = mode.encode && stage_ok && (fused_env || pipelined);
+    if (pipelined && (st = ensure_copy_stream(h, (nq + kChunk - 1) / kChunk)) != QVG_OK) return st;
     if (fused) {
         // K1 runs as the search kernel's per-query prologue
         a.qraw = static_cast<const float*>(din);
         a.qn_out = static_cast<float*>(h->s_qn.p);
         a.qstatus = nullptr;
+        if (pipelined) a.ready = d_ready;
     } else if (mode.encode) {
         launch_encode(static_cast<const float*>(din), nq, ix.dim, ix.Dp,
                       static_cast<float*>(h->s_qn.p), static_cast<uint4*>(h->s_qc.p), nullptr,
@@ -281,6 +322,33 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     }
     cudaEventRecord(h->ev[2], s);
     if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) return st;
+    if (pipelined) {
+        // chunks after the counter / ready reset (ev[1]); each chunk's ready
+        // count is a 4-byte copy ordered after its rows on the same stream
+        cudaStream_t cs = h->copy_stream;
+        cudaStreamWaitEvent(cs, h->ev[1], 0);
+        const size_t row = (size_t)ix.dim * 4;
+        for (uint64_t c0 = 0, c = 0; c0 < nq; c0 += kChunk, ++c) {
+            const uint64_t c1 = c0 + kChunk < nq ? c0 + kChunk : nq;
+            e = cudaMemcpyAsync(static_cast<char*>(h->s_in.p) + c0 * row,
+                                static_cast<const char*>(user_in) + c0 * row, (c1 - c0) * row,
+                                cudaMemcpyHostToDevice, cs);
+            if (e == cudaSuccess) {
+                h->ready_host[c] = (uint32_t)c1;
+                e = cudaMemcpyAsync(d_ready, &h->ready_host[c], 4, cudaMemcpyHostToDevice, cs);
+            }
+            if (e != cudaSuccess) {
+                // never leave the running kernel waiting: release every query
+                launch_set_word(d_ready, (uint32_t)nq, cs);
+                cudaEventRecord(h->ev_copy, cs);
+                cudaStreamWaitEvent(s, h->ev_copy, 0);
+                cudaStreamSynchronize(s);
+                return cuda_status(e, "H2D(queries, pipelined)");
+            }
+        }
+        cudaEventRecord(h->ev_copy, cs);
+        cudaStreamWaitEvent(s, h->ev_copy, 0);
+    }
     cudaEventRecord(h->ev[3], s);
     Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
     for (Out* o : outs) {

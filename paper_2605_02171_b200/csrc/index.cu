@@ -81,6 +81,9 @@ void free_index(qvg_index* h) {
     for (Buffer* b : bufs) cudaFree(b->p);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    if (h->ev_copy) cudaEventDestroy(h->ev_copy);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->ready_host) cudaFreeHost(h->ready_host);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }

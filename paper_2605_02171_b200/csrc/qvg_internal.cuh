@@ -56,6 +56,12 @@ struct qvg_index {
     qvg::Buffer s_in, s_qn, s_qc, s_qst, s_ids, s_sc, s_cnt, s_pool_i, s_pool_d, s_pool_n,
         s_qctr, s_counter, s_exact, s_pair_ids, s_pair_out, s_st;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    // pipelined upload of host queries (created on first use): copy stream,
+    // its completion event, pinned ready counts published after each chunk
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copy = nullptr;
+    uint32_t* ready_host = nullptr;
+    size_t ready_cap = 0;
     // TMA descriptor over the code rows (2-D: 2W u64 columns x n rows, box
     // {2W, 1}) for tile::gather4; valid iff has_tmap (W <= 128)
     alignas(64) CUtensorMap tmap;
@@ -115,6 +121,8 @@ struct SearchLaunch {
     uint64_t exact_words;   // words per slot
     uint32_t depth;         // rerank depth (>= k): the `depth` best scored keys are
                             // reranked; depth == ef is the reference (search.cpp:138)
+    const uint32_t* ready;  // nullable: queries [0, *ready) have landed in qraw
+                            // (pipelined upload; the warp waits before its prologue)
 };
 
 // keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)

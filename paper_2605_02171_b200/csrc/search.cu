@@ -277,8 +277,11 @@ __host__ __device__ inline uint32_t stage_rows_for(uint32_t W, uint32_t RM, uint
 // registers, bounds residency at the BASELINE geometries (R=32 rows -> ~9
 // blocks of 2 warps fit in smem; R=64 -> ~7)
 template <int RW>
+#ifndef QVG_MINBLOCKS_RW2
+#define QVG_MINBLOCKS_RW2 7
+#endif
 struct MinBlocks {
-    static constexpr int value = RW == 1 ? 9 : (RW == 2 ? 7 : 5);
+    static constexpr int value = RW == 1 ? 9 : (RW == 2 ? QVG_MINBLOCKS_RW2 : 5);
 };
 
 // XA: rerank deeper than ef.  A = the best `xa` scored keys outside P, kept
@@ -376,6 +379,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         qq = __shfl_sync(kFull, qq, 0);
         if (qq >= a.nq) break;
         const uint64_t q = qq;
+        if (a.ready) {  // pipelined upload: wait until this query's row has landed
+            if (lane == 0) {
+                uint32_t r;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(a.ready) : "memory");
+                    if (r > q) break;
+                    __nanosleep(256);
+                }
+            }
+            __syncwarp();
+        }
 
         int32_t qst = 0;
         if (a.qraw) {
@@ -388,7 +402,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             const uint32_t dim = ix.dim;
             bool fin = true;
             for (uint32_t i = lane; i < dim; i += 32) {
-                const float v = __ldg(src + i);
+                // L2-only load: with a pipelined upload the row may have been
+                // written by a copy engine during this launch (no stale L1 line)
+                const float v = __ldcg(src + i);
                 fin &= isfinite(v);
                 row[i] = v;
             }
