@@ -256,6 +256,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         auto it = h->plans.find(key);
         if (it == h->plans.end()) {
             if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;
+            pinfo.coop_cap = h->has_tmap ? coop_capacity(a, h->device) : 0;
             it = h->plans.emplace(key, std::make_pair(vlog, pinfo)).first;
         }
         pinfo = it->second.second;
@@ -321,7 +322,23 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         cudaMemsetAsync(h->s_qst.p, 0, nq * 4, s);
     }
     cudaEventRecord(h->ev[2], s);
-    if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) return st;
+    // small batches: one CTA per query (latency mode, search_coop.cu) when the
+    // whole batch fits in one wave of its CTAs (measured: cfg2 batch 1 0.48 ->
+    // 0.39 ms, batch 1024 0.69 -> 0.57 ms; beyond one wave the per-warp kernel
+    // wins, e.g. batch 2048 0.83 vs 1.03 ms).  QVG_COOP_MAX_NQ overrides the
+    // cut-off (0 disables).
+    static const int64_t coop_env = [] {
+        const char* v = getenv("QVG_COOP_MAX_NQ");
+        return v ? (int64_t)strtoll(v, nullptr, 0) : -1ll;
+    }();
+    bool coop = coop_env != 0 && pinfo.coop_cap > 0 && !a.exact_bits && !a.qraw && !a.ready &&
+                !(a.do_rerank && a.depth != a.ef);
+    if (coop) coop = coop_env > 0 ? nq <= (uint64_t)coop_env : nq <= pinfo.coop_cap;
+    if (coop) {
+        if ((st = launch_coop(a, &h->tmap, s, h->device)) != QVG_OK) return st;
+    } else if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) {
+        return st;
+    }
     if (pipelined) {
         // chunks after the counter / ready reset (ev[1]); each chunk's ready
         // count is a 4-byte copy ordered after its rows on the same stream

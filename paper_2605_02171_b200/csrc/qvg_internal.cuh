@@ -38,6 +38,7 @@ struct Buffer {
 
 struct PlanInfo {
     uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0, sms = 0;
+    uint64_t coop_cap = 0;  // resident CTAs of the latency kernel (0 = n/a)
 };
 
 }  // namespace qvg
@@ -141,6 +142,9 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid,
                        PlanInfo* info = nullptr);
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s);
+// latency mode (search_coop.cu): one CTA of warps per query for small batches
+uint64_t coop_capacity(const SearchLaunch& a, int device);  // 0 = not applicable
+qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s, int device);
 // encode the gather4 descriptor for a code table (false if W > 128)
 bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W);
 void launch_pair_distance(const DevIndex& ix, const uint4* qchunks, const uint32_t* ids,

@@ -1,0 +1,140 @@
+// Device helpers shared by the search kernels (search.cu: one warp per query;
+// search_coop.cu: a block of warps per query).  Key layout, visited hash,
+// binary searches and the SM2 row accumulator; see search.cu's header for the
+// algorithm and the reference lines each piece follows.
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+#include "bq_device.cuh"
+
+namespace qvg {
+namespace {
+
+using namespace dev;  // sm2_chunk, TMA / mbarrier wrappers (bq_device.cuh)
+
+constexpr uint64_t kInfKey = ~0ull;
+constexpr uint64_t kExp = 1ull << 32;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint64_t mkkey(uint32_t dist, uint32_t id) {
+    return ((uint64_t)dist << 33) | id;
+}
+__device__ __forceinline__ uint64_t ordk(uint64_t k) { return k & ~kExp; }
+__device__ __forceinline__ uint32_t kdist(uint64_t k) { return (uint32_t)(k >> 33); }
+
+__device__ __forceinline__ uint32_t vhash(uint32_t id, uint32_t lg) {
+    return (id * 0x9E3779B1u) >> (32 - lg);
+}
+
+
+// column 0 (code rows are one TMA box wide)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint32_t r0,
+                                            uint32_t r1, uint32_t r2, uint32_t r3,
+                                            uint64_t* bar) {
+    dev::tma_gather4(dst, map, 0, r0, r1, r2, r3, bar);
+}
+__device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* map, uint32_t col,
+                                                uint32_t r0, uint32_t r1, uint32_t r2,
+                                                uint32_t r3, uint64_t* bar) {
+    dev::tma_gather4(dst, map, col, r0, r1, r2, r3, bar);
+}
+
+// Row distance accumulator in bit planes (Harley-Seal carry-save adders).
+// Per chunk the SM2 terms are four weight-1 words (x0, x1, o0, o1) and two
+// weight-2 words (a0, a1) (encoding.hpp:169-176: popc(x) + popc(x & (sa|sb)) +
+// 2 popc(x & sa & sb)).  Adding them through CSAs (LOP3s on the ALU pipe)
+// leaves one POPC per chunk instead of six: POPC runs on the XU pipe at a
+// quarter of the ALU rate on B200 (tools/popc_bench.cu: 0.5 vs 2 warp-ops per
+// SM per cycle), and the XU pipe was the busiest in the search kernel.
+__device__ __forceinline__ void csa(uint32_t& a, uint32_t b, uint32_t c, uint32_t& carry) {
+    const uint32_t u = a ^ b;
+    carry = (a & b) | (u & c);
+    a = u ^ c;
+}
+struct Sm2Acc {
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, d16 = 0;
+    __device__ __forceinline__ void add(const uint4 q, const uint4 v) {
+        const uint32_t x0 = q.x ^ v.x, x1 = q.y ^ v.y;
+        const uint32_t o0 = x0 & (q.z | v.z), o1 = x1 & (q.w | v.w);
+        const uint32_t a0 = x0 & q.z & v.z, a1 = x1 & q.w & v.w;
+        uint32_t c1, c2, f1, f2, e;
+        csa(ones, x0, x1, c1);   // weight 1 -> carries of weight 2
+        csa(ones, o0, o1, c2);
+        csa(twos, c1, c2, f1);   // weight 2 -> carries of weight 4
+        csa(twos, a0, a1, f2);
+        csa(fours, f1, f2, e);   // weight 4 -> carry of weight 8
+        d16 += __popc(eights & e);  // half adder at weight 8, carry counted
+        eights ^= e;
+    }
+    __device__ __forceinline__ uint32_t total() const {
+        return __popc(ones) + 2u * __popc(twos) + 4u * __popc(fours) + 8u * __popc(eights) +
+               16u * d16;
+    }
+};
+
+// SM2 distance of one staged row, taken by one of the LPR lanes that share
+// the row: part p (t = p, p+LPR, ... < W) reads chunk (rot + t - p) mod W,
+// rot = lane mod W — the per-lane rotation that keeps the 8 lanes of an
+// LDS.128 phase on distinct bank quads.  One lockstep loop (a per-lane wrap
+// point must not become a branch: divergent segments cost +50 %), unrolled by
+// 4 with the four chunk indices computed first so the eight loads can issue
+// together.
+__device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
+                                            const uint4* __restrict__ row, uint32_t W,
+                                            uint32_t rot, uint32_t part, uint32_t LPR) {
+    Sm2Acc acc;
+    const uint32_t iters = (W - part + LPR - 1) / LPR;
+    uint32_t cc = rot, i = 0;
+    auto nxt = [&](uint32_t x) {
+        x += LPR;
+        return x >= W ? x - W : x;
+    };
+    for (; i + 4 <= iters; i += 4) {
+        const uint32_t c0 = cc, c1 = nxt(c0), c2 = nxt(c1), c3 = nxt(c2);
+        cc = nxt(c3);
+        const uint4 q0 = qc[c0], v0 = row[c0], q1 = qc[c1], v1 = row[c1];
+        const uint4 q2 = qc[c2], v2 = row[c2], q3 = qc[c3], v3 = row[c3];
+        acc.add(q0, v0);
+        acc.add(q1, v1);
+        acc.add(q2, v2);
+        acc.add(q3, v3);
+    }
+    for (; i < iters; ++i) {
+        acc.add(qc[cc], row[cc]);
+        cc = nxt(cc);
+    }
+    return acc.total();
+}
+
+// first index i in [0, n) with ordk(a[i]) >= x
+__device__ __forceinline__ uint32_t lower_bound_key(const uint64_t* a, uint32_t n, uint64_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ordk(a[mid]) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// #{j < m : a[j] <= x} for non-decreasing a
+__device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t m, uint32_t x) {
+    uint32_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+
+// bytes of one 4-row TMA group in the stage; gather4 destinations must be
+// 128-B aligned, so groups are padded (row j of a half lives at
+// (j/4)*group_stride + (j%4)*16W)
+__host__ __device__ inline uint32_t group_stride(uint32_t W) { return (64u * W + 127u) & ~127u; }
+
+}  // namespace
+}  // namespace qvg

@@ -145,11 +145,12 @@ print("OK")
                                  {"QVG_VARIANT": "13"}, {"QVG_STAGE_HALF_BYTES": "512"},
                                  {"QVG_SPLIT_MAX_ROWS": "32"},
                                  {"QVG_SPLIT_MAX_ROWS": "32", "QVG_STAGE_HALF_BYTES": "512"},
-                                 {"QVG_SPLIT_MAX_ROWS": "0"}])
+                                 {"QVG_SPLIT_MAX_ROWS": "0"}, {"QVG_COOP_MAX_NQ": "1000000"}])
 def test_opt_in_variants_match_golden(env):
     """The opt-in kernel variants (env switches read once per process): fused
     encode prologue, tiled / block encoders, paired distance pass, LDG rerank
-    fallback (+ no-allocate loads, no L2 prefetch), tiny stage.  All bit-exact."""
+    fallback (+ no-allocate loads, no L2 prefetch), tiny stage, forced row
+    splitting, and the one-CTA-per-query latency kernel.  All bit-exact."""
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
