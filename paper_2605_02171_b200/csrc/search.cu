@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         uint64_t* bar = &bars[h];
         const uint32_t ng = use_tmap ? (cnt + 3u) >> 2 : cnt;
         const uint32_t bytes = use_tmap ? ng * 4u * rowb : cnt * rowb;
-        fence_proxy_async();  // order this lane's reads of the half before TMA writes
+        TMA_WAR_FENCE();  // order this lane's reads of the half before TMA writes
         __syncwarp();         // all lanes finished reading this half
         if (lane == 0) mbar_expect_tx(bar, bytes);
         __syncwarp();

@@ -14,6 +14,13 @@ namespace {
 
 using namespace dev;  // sm2_chunk, TMA / mbarrier wrappers (bq_device.cuh)
 
+// cross-proxy WAR fence before a TMA overwrites a stage the warp has read
+#ifdef QVG_NO_TMA_FENCE
+#define TMA_WAR_FENCE() ((void)0)
+#else
+#define TMA_WAR_FENCE() fence_proxy_async()
+#endif
+
 constexpr uint64_t kInfKey = ~0ull;
 constexpr uint64_t kExp = 1ull << 32;
 constexpr unsigned kFull = 0xFFFFFFFFu;

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
             const uint32_t cnt = n > r0 ? min(SRW, n - r0) : 0u;
             if (cnt) {
                 const uint32_t ng = (cnt + 3u) >> 2;
-                fence_proxy_async();
+                TMA_WAR_FENCE();
                 __syncwarp();
                 if (lane == 0) mbar_expect_tx(bar, ng * 4u * rowb);
                 __syncwarp();
