@@ -190,6 +190,8 @@ def algorithmic_bytes(st, W, D, k, nq):
 def recall_at_k(res, gt, k):
     """eval.cpp:171-195"""
     tot = 0.0
+    if gt is None or len(res) == 0:
+        return None
     for r, g in zip(res, gt):
         gs = set(int(x) for x in g[:k])
         tot += sum(1 for x in r[:k] if int(x) in gs) / k
@@ -322,12 +324,14 @@ def ours(args):
 
     # ---- recall (GPU fp32 brute force on a sample) ---------------------------
     rq = min(args.recall_queries, nq)
-    base_dev = torch.from_numpy(qn).cuda()
-    qnq, _, _ = Q.encode_queries(queries[:rq], device=local)  # normalised like query()
-    # exact ground truth on the GPU: qivr::brute_force_topk(float_cosine)
-    # semantics (4-chain double dot, ties by id) via qvg_brute_force_topk
-    gt = Q.brute_force_topk(base_dev, torch.from_numpy(qnq).cuda(), k, device=local)
-    del base_dev
+    gt = None
+    if rq > 0:
+        base_dev = torch.from_numpy(qn).cuda()
+        qnq, _, _ = Q.encode_queries(queries[:rq], device=local)  # normalised like query()
+        # exact ground truth on the GPU: qivr::brute_force_topk(float_cosine)
+        # semantics (4-chain double dot, ties by id) via qvg_brute_force_topk
+        gt = Q.brute_force_topk(base_dev, torch.from_numpy(qnq).cuda(), k, device=local)
+        del base_dev
     recall = recall_at_k(ex["ids"][:rq], gt, k)
 
     # ---- ef sweep ------------------------------------------------------------

@@ -97,11 +97,6 @@ struct Mode {
     bool rerank;
 };
 
-__global__ void set_word_kernel(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-void launch_set_word(uint32_t* p, uint32_t v, cudaStream_t s) { set_word_kernel<<<1, 1, 0, s>>>(p, v); }
-
 // copy stream, its event and `chunks` pinned ready slots for the pipelined upload
 qvg_status ensure_copy_stream(qvg_index* h, uint64_t chunks) {
     cudaError_t e;
@@ -334,14 +329,14 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     bool coop = coop_env != 0 && pinfo.coop_cap > 0 && !a.exact_bits && !a.qraw && !a.ready &&
                 !(a.do_rerank && a.depth != a.ef);
     if (coop) coop = coop_env > 0 ? nq <= (uint64_t)coop_env : nq <= pinfo.coop_cap;
-    if (coop) {
-        if ((st = launch_coop(a, &h->tmap, s, h->device)) != QVG_OK) return st;
-    } else if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) {
-        return st;
-    }
     if (pipelined) {
-        // chunks after the counter / ready reset (ev[1]); each chunk's ready
-        // count is a 4-byte copy ordered after its rows on the same stream
+        // The chunk copies are submitted BEFORE the search launch: in normal
+        // operation the copy engine still overlaps them with the running
+        // kernel (each warp waits only for its own query's chunk), and a tool
+        // that serialises launches (ncu kernel replay, compute-sanitizer)
+        // drains them before the kernel starts instead of deadlocking it.
+        // Each chunk's ready count is a 4-byte copy ordered after its rows on
+        // the copy stream; the chunks start after the counter reset (ev[1]).
         cudaStream_t cs = h->copy_stream;
         cudaStreamWaitEvent(cs, h->ev[1], 0);
         const size_t row = (size_t)ix.dim * 4;
@@ -355,17 +350,18 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
                 e = cudaMemcpyAsync(d_ready, &h->ready_host[c], 4, cudaMemcpyHostToDevice, cs);
             }
             if (e != cudaSuccess) {
-                // never leave the running kernel waiting: release every query
-                launch_set_word(d_ready, (uint32_t)nq, cs);
-                cudaEventRecord(h->ev_copy, cs);
-                cudaStreamWaitEvent(s, h->ev_copy, 0);
-                cudaStreamSynchronize(s);
+                cudaStreamSynchronize(cs);  // no kernel was launched yet: nothing waits
                 return cuda_status(e, "H2D(queries, pipelined)");
             }
         }
         cudaEventRecord(h->ev_copy, cs);
-        cudaStreamWaitEvent(s, h->ev_copy, 0);
     }
+    if (coop) {
+        if ((st = launch_coop(a, &h->tmap, s, h->device)) != QVG_OK) return st;
+    } else if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) {
+        return st;
+    }
+    if (pipelined) cudaStreamWaitEvent(s, h->ev_copy, 0);  // results after every chunk
     cudaEventRecord(h->ev[3], s);
     Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
     for (Out* o : outs) {
