@@ -8,12 +8,15 @@
 //   encode_sm2_into        encoding.cpp:32-45  (pos = y > 0, strong = |y| > tau,
 //                          strict, pad bits zero)
 // The double reductions must run in index order to round identically, so one
-// lane owns one query; the batch supplies the parallelism.  A warp owns 32
-// consecutive queries and moves data through a transposed shared-memory tile,
-// so every global load/store instruction covers 128 contiguous bytes of one
-// row (a thread-per-row layout would touch 32 lines per instruction).  All
-// arithmetic uses explicit _rn intrinsics so no contraction can change a
+// lane owns one query's chain and the batch supplies the parallelism.
+// Kernels (QVG_ENCODE selects; all bit-exact, tests/test_gpu_parity.py):
+//   0 encode_lpq_kernel   (default) lane per query, rows staged in shared memory
+//   1 encode_tiled_kernel lane per query through 32x32 transposed tiles
+//   2 encode_warp_kernel  warp per query, lane 0 runs the chains
+//   3 encode_block_kernel lane per query, TMA-staged block of rows
+// All arithmetic uses explicit _rn intrinsics so no contraction can change a
 // rounding.
+#include <algorithm>
 #include <cstdlib>
 
 #include "qvg_internal.cuh"
@@ -119,6 +122,127 @@ __global__ void __launch_bounds__(128) encode_tiled_kernel(
         status[myq] = st;
         if (st != QVG_Q_OK && flags) atomicOr(flags, 1u << st);
         if (tau_out) tau_out[myq] = tau;
+    }
+}
+
+// Lane-per-query (default): a block of 128 threads owns QB <= 32 consecutive
+// queries staged in shared memory with an odd row stride ld (at step i lane q
+// reads word q*ld + i: 32 distinct banks).  Lane q of warp 0 runs query q's two
+// index-ordered double reductions, so one FP64 warp-instruction advances 32
+// chains: the FP64 pipe issues ~0.5 warp-instructions per clock per SM on the
+// B200 whatever the active-lane count (tools/fp64_chain_bench.cu), so a lane-0
+// chain per query leaves 31/32 of it idle and throughput-bound.  Staging,
+// scaling, the qn stores and the bit packing (two ballots per 32 elements) are
+// element-parallel over the block's four warps.
+constexpr uint32_t kLpqThreads = 128;
+
+__device__ __forceinline__ uint32_t lpq_ld(uint32_t dim) { return dim | 1u; }
+
+__global__ void __launch_bounds__(kLpqThreads) encode_lpq_kernel(
+    const float* __restrict__ x, uint64_t nq, uint32_t dim, uint32_t Dp, uint32_t QB,
+    float* __restrict__ qn, uint4* __restrict__ qcodes, float* __restrict__ tau_out,
+    int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
+    extern __shared__ float rows[];  // QB x ld
+    __shared__ float s_inv[32], s_tau[32];
+    __shared__ int32_t s_st[32], s_bad[32], s_ybad[32];
+    constexpr uint32_t kWarps = kLpqThreads / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t q0 = (uint64_t)blockIdx.x * QB;
+    const uint32_t nb = (uint32_t)min((uint64_t)QB, nq - q0);
+    const uint32_t ld = lpq_ld(dim);
+    if (tid < 32) s_bad[tid] = s_ybad[tid] = 0;
+    __syncthreads();
+    // stage the rows (warp per row, coalesced) + finite check (search.cpp:128-131)
+    for (uint32_t r = wid; r < nb; r += kWarps) {
+        const float* src = x + (q0 + r) * dim;
+        float* row = rows + (size_t)r * ld;
+        bool bad = false;
+#pragma unroll 4
+        for (uint32_t i = lane; i < dim; i += 32) {
+            const float v = __ldg(src + i);
+            bad |= !isfinite(v);
+            row[i] = v;
+        }
+        bad = __any_sync(0xFFFFFFFFu, bad);
+        if (lane == 0 && bad) s_bad[r] = 1;
+    }
+    __syncthreads();
+    // chain 1 (vec_math.hpp:28-44): sum of squares in index order; x*x is
+    // exact in double, so the FMA rounds exactly like acc + x*x
+    if (wid == 0 && lane < nb) {
+        int32_t st = s_bad[lane] ? QVG_Q_NONFINITE_COORD : QVG_Q_OK;
+        float inv = 0.0f;
+        if (st == QVG_Q_OK) {
+            const float* row = rows + (size_t)lane * ld;
+            double acc = 0.0;
+#pragma unroll 8
+            for (uint32_t i = 0; i < dim; ++i) acc = __fma_rn((double)row[i], (double)row[i], acc);
+            const double norm = __dsqrt_rn(acc);
+            if (!(norm > 0.0) || isinf(norm)) st = QVG_Q_BAD_NORM;
+            else inv = __double2float_rn(__ddiv_rn(1.0, norm));
+        }
+        s_st[lane] = st;
+        s_inv[lane] = inv;
+    }
+    __syncthreads();
+    // y = x * inv (f32), in place; qn row with zero padding to Dp
+    for (uint32_t r = wid; r < nb; r += kWarps) {
+        const bool ok = s_st[r] == QVG_Q_OK;
+        const float inv = s_inv[r];
+        float* row = rows + (size_t)r * ld;
+        float* dst = qn + (q0 + r) * Dp;
+        bool bad = false;
+#pragma unroll 4
+        for (uint32_t i = lane; i < Dp; i += 32) {
+            float y = 0.0f;
+            if (i < dim) {
+                y = ok ? __fmul_rn(row[i], inv) : 0.0f;
+                bad |= !isfinite(y);
+                row[i] = y;
+            }
+            dst[i] = y;
+        }
+        bad = __any_sync(0xFFFFFFFFu, bad);
+        if (lane == 0 && bad) s_ybad[r] = 1;
+    }
+    __syncthreads();
+    // chain 2 (encoding.cpp:23-30): tau = float(sum |y| / D), index order
+    if (wid == 0 && lane < nb) {
+        int32_t st = s_st[lane];
+        if (st == QVG_Q_OK && s_ybad[lane]) st = QVG_Q_NONFINITE_CODE;
+        float tau = 0.0f;
+        if (st == QVG_Q_OK) {
+            const float* row = rows + (size_t)lane * ld;
+            double s = 0.0;
+#pragma unroll 8
+            for (uint32_t i = 0; i < dim; ++i) s = __dadd_rn(s, fabs((double)row[i]));
+            tau = __double2float_rn(__ddiv_rn(s, (double)dim));
+        }
+        s_st[lane] = st;
+        s_tau[lane] = tau;
+        const uint64_t q = q0 + lane;
+        status[q] = st;
+        if (st != QVG_Q_OK && flags) atomicOr(flags, 1u << st);
+        if (tau_out) tau_out[q] = tau;
+    }
+    __syncthreads();
+    // bit planes (encode_sm2_into, encoding.cpp:32-45): warp per (row, 64-bit
+    // word), lane b of each half sets bit b; pad bits and failed rows zero
+    const uint32_t W = (dim + 63) / 64;
+    for (uint32_t t = wid; t < nb * W; t += kWarps) {
+        const uint32_t r = t / W, w = t - r * W;
+        const bool ok = s_st[r] == QVG_Q_OK;
+        const float tau = s_tau[r];
+        const float* row = rows + (size_t)r * ld;
+        uint32_t pb[2], sb[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t i = w * 64 + h * 32 + lane;
+            const float y = (ok && i < dim) ? row[i] : 0.0f;
+            pb[h] = __ballot_sync(0xFFFFFFFFu, y > 0.0f);
+            sb[h] = __ballot_sync(0xFFFFFFFFu, ok && i < dim && fabsf(y) > tau);
+        }
+        if (lane == 0) qcodes[(q0 + r) * W + w] = make_uint4(pb[0], pb[1], sb[0], sb[1]);
     }
 }
 
@@ -361,6 +485,38 @@ void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float
         encode_block_kernel<<<blocks, 32, bsmem, s>>>(x, nq, dim, Dp, QB, qn, qcodes, tau, status,
                                                        flags);
         return;
+    }
+    if (variant == 0) {
+        // largest QB (<= 32 queries per block) that still fits the batch in one
+        // wave of resident blocks; QB = 32 when no QB does (large batches)
+        static int sms = [] {
+            int d = 0, v = 0;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+            return v > 0 ? v : 1;
+        }();
+        const size_t row_bytes = (size_t)(dim | 1u) * 4;
+        const size_t cap = 200u * 1024u;
+        uint32_t qb = 0;
+        for (uint32_t c = 32; c >= 4; --c) {
+            const size_t sm = row_bytes * c;
+            if (sm > cap) continue;
+            const uint64_t per_sm = std::min<uint64_t>(227u * 1024u / (sm + 1024u), 16u);
+            if (!qb) qb = c;  // largest that fits in shared memory
+            if ((nq + c - 1) / c <= per_sm * (uint64_t)sms) {
+                qb = c;
+                break;
+            }
+        }
+        if (qb) {
+            const size_t lsmem = row_bytes * qb;
+            cudaFuncSetAttribute(encode_lpq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lsmem);
+            const unsigned blocks = (unsigned)((nq + qb - 1) / qb);
+            encode_lpq_kernel<<<blocks, kLpqThreads, lsmem, s>>>(x, nq, dim, Dp, qb, qn, qcodes,
+                                                                 tau, status, flags);
+            return;
+        }
     }
     if (variant == 1 || smem > 200 * 1024) {
         const unsigned blocks = (unsigned)((nq + 127) / 128);
