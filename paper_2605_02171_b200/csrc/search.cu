@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     uint32_t lpr_log = 0;
     while (SPLIT && (SR << (lpr_log + 1)) <= 32u) ++lpr_log;
     const uint32_t LPR = SPLIT ? 1u << lpr_log : 1u;
+    constexpr bool ctd_prefetch = true;  // prefetch the best contender's adjacency row
 
     if (lane == 0) {
         mbar_init(&bars[0]);
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         if (lane == 0) cid[0] = entry;
         __syncwarp();
         uint32_t spec_u = kSentinel;  // speculatively prefetched adjacency row
+        uint64_t spec_key = kInfKey;  // its key (the predicted next pick)
         uint32_t spec_v[RW];
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
@@ -418,12 +420,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             // entry (the next pick unless this row inserts a better one)
             {
                 uint32_t guess = kSentinel;
+                spec_key = kInfKey;
                 for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
                     const uint32_t idx = b0 + lane;
                     const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
                     const unsigned bal = __ballot_sync(kFull, un);
                     if (bal) {
-                        guess = (uint32_t)pk[b0 + __ffs(bal) - 1];
+                        spec_key = ordk(pk[b0 + __ffs(bal) - 1]);
+                        guess = (uint32_t)spec_key;
                         break;
                     }
                 }
@@ -475,6 +479,38 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     crp[pos] = rp;
                 }
                 m += __popc(bal);
+                if (ctd_prefetch && bal) {
+                    // the smallest contender is always admitted (no smaller
+                    // earlier contender, and it beats max(P)); if it also beats
+                    // the predicted pick it becomes the next pick: fetch its
+                    // adjacency row now, under the remaining distance work
+                    const uint32_t dmin = __reduce_min_sync(kFull, c ? d : ~0u);
+                    const uint32_t imin = __reduce_min_sync(kFull, (c && d == dmin) ? id : ~0u);
+                    const uint64_t kmin = mkkey(dmin, imin);
+                    if (kmin < spec_key) {
+                        spec_key = kmin;
+                        spec_u = imin;
+                        const uint32_t* row = ix.adj + (size_t)imin * ix.RS;
+                        if (lane * RW < ix.RS) {
+                            if (RW == 1) {
+                                spec_v[0] = __ldg(row + lane);
+                            } else if (RW == 2) {
+                                const uint2 t = __ldg(reinterpret_cast<const uint2*>(row) + lane);
+                                spec_v[0] = t.x;
+                                spec_v[RW - 1] = t.y;
+                            } else {
+                                const uint4 t = __ldg(reinterpret_cast<const uint4*>(row) + lane);
+                                spec_v[0] = t.x;
+                                spec_v[1 % RW] = t.y;
+                                spec_v[2 % RW] = t.z;
+                                spec_v[3 % RW] = t.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < RW; ++j) spec_v[j] = kSentinel;
+                        }
+                    }
+                }
                 if constexpr (XA) {
                     // above max(P) (key == max(P) is P's own entry) and below
                     // max(A); a key already in A is a visited-table miss
