@@ -222,6 +222,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
     uint32_t lpr_log = 0;
     while (SPLIT && (SR << (lpr_log + 1)) <= 32u) ++lpr_log;
     const uint32_t LPR = SPLIT ? 1u << lpr_log : 1u;
+    // x / SR == __umulhi(x, sr_m) for x < 2^32 / SR (x <= a few hundred here)
+    const uint32_t sr_m = 0xFFFFFFFFu / SR + 1u;
     constexpr bool ctd_prefetch = true;  // prefetch the best contender's adjacency row
 
     if (lane == 0) {
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    uint32_t phase0 = 0, phase1 = 0;
+    uint32_t phs = 0;  // bit h = phase parity of bars[h]
 
     // issue the TMA fetch of compacted rows [r0, r0+cnt) into stage half h
     auto issue = [&](uint32_t r0, uint32_t cnt, uint32_t h) {
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             QVG_PH(long long tp0 = clock64();)
             c_eval += n;
             // (a) TMA-gather the code rows (double-buffered halves of SR rows)
-            const uint32_t nsub = (n + SR - 1) / SR;
+            const uint32_t nsub = __umulhi(n + SR - 1, sr_m);  // (n + SR - 1) / SR
             if (nsub > 0) issue(0, min(n, SR), 0);
             if (nsub > 1) issue(SR, min(n - SR, SR), 1);
             QVG_PH(ph_tma += clock64() - tp0;)
@@ -534,12 +536,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 // Chunks are visited from a per-lane rotation (bank spreading) as
                 // two straight ranges [rot, W) and [0, rot).
                 for (uint32_t k = 0; k < nsub; k += 2) {
-                    mbar_wait(&bars[0], phase0);
-                    phase0 ^= 1u;
+                    mbar_wait(&bars[0], phs & 1u);
+                    phs ^= 1u;
                     const bool two = k + 1 < nsub;
                     if (two) {
-                        mbar_wait(&bars[1], phase1);
-                        phase1 ^= 1u;
+                        mbar_wait(&bars[1], (phs >> 1) & 1u);
+                        phs ^= 2u;
                     }
                     const uint32_t cnt0 = min(n - k * SR, SR);
                     const uint32_t cnt1 = two ? min(n - (k + 1) * SR, SR) : 0u;
@@ -576,13 +578,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             for (uint32_t k = 0; !paired && k < nsub; ++k) {
                 const uint32_t h = k & 1u;
                 QVG_PH(long long tw0 = clock64();)
-                if (h == 0) {
-                    mbar_wait(&bars[0], phase0);
-                    phase0 ^= 1u;
-                } else {
-                    mbar_wait(&bars[1], phase1);
-                    phase1 ^= 1u;
-                }
+                mbar_wait(&bars[h], (phs >> h) & 1u);
+                phs ^= 1u << h;
                 QVG_PH(ph_wait += clock64() - tw0;)
                 const uint32_t r0 = k * SR;
                 const uint32_t cnt = min(n - r0, SR);
@@ -909,10 +906,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 const uint32_t dim = ix.dim;
                 const uint32_t main4 = dim & ~3u;
                 const uint32_t nsl = (dim + SL - 1) / SL;
+                const uint32_t nsl_m = 0xFFFFFFFFu / nsl + 1u;  // t / nsl == __umulhi(t, nsl_m)
                 const uint32_t rounds = ((NR + 31) / 32) * nsl;
                 const uint32_t cgs = (16u * SL + 127u) & ~127u;  // bytes per 4-row group
                 auto rr_issue = [&](uint32_t t) {
-                    const uint32_t g = t / nsl, s = t % nsl, h = t & 1u;
+                    const uint32_t g = __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
                     const uint32_t rows = min(32u, NR - 32u * g);
                     const uint32_t ng4 = (rows + 3u) >> 2;
                     // the query slice rides in the same transaction (16-B multiple,
@@ -940,7 +938,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 if (rounds > 1) rr_issue(1);
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 for (uint32_t t = 0; t < rounds; ++t) {
-                    const uint32_t g = t / nsl, s = t % nsl, h = t & 1u;
+                    const uint32_t g = __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
                     // the round's query slice -> registers in one batch of
                     // independent loads, issued before the stage wait (qn is
                     // L2-resident; L1 is mostly carved out for shared memory)
@@ -948,13 +946,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     const uint32_t i0 = s * SL;
                     const uint32_t lim = min(SL, dim - i0);
                     const float4* qr = reinterpret_cast<const float4*>(qsl) + h * (kMaxSL4);
-                    if (h == 0) {
-                        mbar_wait(&bars[0], phase0);
-                        phase0 ^= 1u;
-                    } else {
-                        mbar_wait(&bars[1], phase1);
-                        phase1 ^= 1u;
-                    }
+                    mbar_wait(&bars[h], (phs >> h) & 1u);
+                    phs ^= 1u << h;
                     if (s == 0) s0 = s1 = s2 = s3 = 0.0;
                     const uint32_t row = 32u * g + lane;
                     if (row < NR) {
