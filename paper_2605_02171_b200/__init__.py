@@ -244,7 +244,7 @@ class GpuIndex:
         pn = np.empty(nq, np.uint32) if pools else None
         ctr = np.empty((nq, 8), np.uint32) if counters else None
         st = N.qvg_stats()
-        rc = N.lib().qvg_search_ex(self._h, q.ctypes.data, nq, k, ef, C.byref(opts),
+        rc = N.lib().qvg_search_ex(self._h, N.ptr(q), nq, k, ef, C.byref(opts),
                                    ids.ctypes.data if rerank else None,
                                    sc.ctypes.data if rerank else None,
                                    cnt.ctypes.data if rerank else None, qs.ctypes.data,

@@ -1,6 +1,9 @@
 """One warm-up + one measured search launch on a config graph (for ncu).
 
-    ncu -k regex:search_kernel -s 1 -c 1 ... python tools/one_launch.py CONFIG [NQ] [EF]
+    ncu -k regex:search_kernel -s 1 -c 1 ... python tools/one_launch.py CONFIG [NQ] [EF] [dev]
+
+`dev`: queries already in HBM (the bench's `value` path: separate encode
+kernel); default: host queries (pipelined upload + fused encode prologue).
 """
 import os
 import sys
@@ -25,6 +28,9 @@ if g is None:
 qn, codes, _ = Q.encode_queries(base)
 ix = Q.GpuIndex.from_arrays(codes, g["adj"], qn, int(g["entry"]))
 del qn, codes
+if len(sys.argv) > 4 and sys.argv[4] == "dev":
+    import torch
+    queries = torch.from_numpy(queries).cuda()
 for _ in range(2):
     r = ix.search_ex(queries, k=10, ef=ef, pools=False, counters=False)
 print("search_ms", r["stats"]["search_ms"])
