@@ -383,6 +383,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
 
         // ---- per-query init --------------------------------------------------
         const long long t_start = clock64();  // phase timers (variant bit 4: debug)
+#ifdef QVG_TAIL  // occupancy-over-time build (tools/tail_profile.py): wall-clock span per query
+        unsigned long long tg0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
+#endif
         if (!a.qraw)
             for (uint32_t w = lane; w < W; w += 32) qc[w] = a.qcodes[q * W + w];
         if (xbits) {
@@ -1018,6 +1022,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                 a.qctr[q * 8 + 2] = (uint32_t)((clock64() - t_dots) >> 4);
 #endif
         }
+#ifdef QVG_TAIL
+        if (lane == 0 && a.qctr) {
+            unsigned long long tg1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg1));
+            a.qctr[q * 8 + 0] = (uint32_t)tg0;
+            a.qctr[q * 8 + 1] = (uint32_t)tg1;
+            a.qctr[q * 8 + 2] = (uint32_t)gwarp;
+            a.qctr[q * 8 + 3] = blockIdx.x;
+        }
+#endif
         __syncwarp();
     }
 }
