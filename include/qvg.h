@@ -114,7 +114,12 @@ typedef struct qvg_search_opts {
                              * scored nodes.  GPU-only knob (BASELINE config 4), no
                              * reference counterpart; depth <= ef reranks a pool
                              * prefix. */
-    uint32_t reserved[1];
+    uint32_t relaxed_expansions; /* 0 or 1: exact search (the reference).  2 or 4: the
+                             * RELAXED variant — expand that many best unexpanded pool
+                             * entries per step, merge-then-truncate admission, no
+                             * tie stack; NOT result-identical to the reference
+                             * (reported separately).  Needs relaxed * ceil(R/32) <= 4
+                             * and rerank_depth == 0. */
 } qvg_search_opts;
 
 const char* qvg_last_error(void);

@@ -226,15 +226,18 @@ class GpuIndex:
 
     def search_ex(self, queries, k=10, ef=64, visited_slots=0, tie_capacity=0,
                   exact_visited=False, entry_point=None, rerank=True, pools=True,
-                  counters=True, check=True, rerank_depth=0):
+                  counters=True, check=True, rerank_depth=0, relaxed=0):
         """Everything: results, per-query status, pool (ids+dists), counters, stats.
-        rerank_depth (GPU-only, 0 = ef): rerank the best `rerank_depth` scored keys."""
+        rerank_depth (GPU-only, 0 = ef): rerank the best `rerank_depth` scored keys.
+        relaxed (GPU-only, 0 = exact): 2 or 4 expansions per step, merge-then-truncate
+        admission, no tie stack — NOT identical to the reference (reported separately)."""
         q = _f32(queries, self.dim)
         nq = q.shape[0]
         opts = N.qvg_search_opts(visited_slots=visited_slots, tie_capacity=tie_capacity,
                                  exact_visited=int(exact_visited),
                                  entry_point=SENTINEL if entry_point is None else entry_point,
-                                 no_rerank=int(not rerank), rerank_depth=rerank_depth)
+                                 no_rerank=int(not rerank), rerank_depth=rerank_depth,
+                                 relaxed_expansions=relaxed)
         ids = np.empty((nq, k), np.uint32)
         sc = np.empty((nq, k), np.float32)
         cnt = np.empty(nq, np.uint32)

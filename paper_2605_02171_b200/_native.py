@@ -50,7 +50,7 @@ class qvg_search_opts(C.Structure):
     _fields_ = [("visited_slots", C.c_uint32), ("tie_capacity", C.c_uint32),
                 ("exact_visited", C.c_uint32), ("entry_point", C.c_uint32),
                 ("no_rerank", C.c_uint32), ("timing_only", C.c_uint32),
-                ("rerank_depth", C.c_uint32), ("reserved", C.c_uint32 * 1)]
+                ("rerank_depth", C.c_uint32), ("relaxed_expansions", C.c_uint32)]
 
 
 class qvg_build_params(C.Structure):

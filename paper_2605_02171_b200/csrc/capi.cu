@@ -165,6 +165,23 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     }
     uint32_t tcap = opts && opts->tie_capacity ? opts->tie_capacity : (ef < 64 ? 64u : ef);
     tcap = (tcap + 3) & ~3u;
+    // relaxed variant: 0/1 = exact
+    uint32_t relax = opts && opts->relaxed_expansions > 1 ? opts->relaxed_expansions : 0u;
+    if (relax) {
+        if (relax != 2 && relax != 4) {
+            set_error("search: relaxed_expansions must be 0, 1, 2 or 4");
+            return QVG_INVALID_ARGUMENT;
+        }
+        if (!relaxed_rw(ix.R, relax)) {
+            set_error("search: relaxed_expansions * ceil(max_degree / 32) must be <= 4");
+            return QVG_INVALID_ARGUMENT;
+        }
+        if (opts->rerank_depth && opts->rerank_depth != ef) {
+            set_error("search: relaxed_expansions does not combine with rerank_depth");
+            return QVG_INVALID_ARGUMENT;
+        }
+        tcap = 0;  // no tie stack
+    }
     const bool do_rerank = mode.rerank && !(opts && opts->no_rerank);
     // rerank depth (GPU-only knob): 0 = ef, the reference
     const uint32_t depth = opts && opts->rerank_depth ? opts->rerank_depth : ef;
@@ -175,7 +192,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     const uint32_t xa = do_rerank ? extra_depth(ef, depth) : 0u;
     uint32_t vslots = opts && opts->visited_slots ? opts->visited_slots : 0;
     uint32_t vlog;
-    auto cached = h->plans.find(qvg_index::PlanKey{ef, tcap, vslots, xa});
+    auto cached = h->plans.find(qvg_index::PlanKey{ef, tcap, vslots, xa, relax});
     if (cached != h->plans.end()) {
         vlog = cached->second.first;
     } else if (vslots) {
@@ -186,7 +203,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         if (vlog < 5) vlog = 5;
     } else {
         // largest table that keeps the most resident warps (occupancy-aware)
-        vlog = auto_visited_log2(ix, ef, tcap, h->device, xa);
+        vlog = auto_visited_log2(ix, ef, tcap, h->device, xa, relax);
     }
     const bool exact = opts && opts->exact_visited;
     const bool want_ctr = out_qctr != nullptr || (stats && !(opts && opts->timing_only));
@@ -222,6 +239,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     a.entry = entry;
     a.vis_log2 = vlog;
     a.tie_cap = tcap;
+    a.relax = relax;
     a.do_rerank = do_rerank;
     a.depth = ef + xa;
     if (do_rerank && depth < ef) a.depth = depth;
@@ -247,7 +265,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     PlanInfo pinfo;
     {
         const uint32_t vreq = opts && opts->visited_slots ? opts->visited_slots : 0u;
-        const qvg_index::PlanKey key{ef, tcap, vreq, xa};
+        const qvg_index::PlanKey key{ef, tcap, vreq, xa, relax};
         auto it = h->plans.find(key);
         if (it == h->plans.end()) {
             if ((st = plan_search(a, h->device, &grid, &pinfo)) != QVG_OK) return st;
@@ -327,7 +345,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         return v ? (int64_t)strtoll(v, nullptr, 0) : -1ll;
     }();
     bool coop = coop_env != 0 && pinfo.coop_cap > 0 && !a.exact_bits && !a.qraw && !a.ready &&
-                !(a.do_rerank && a.depth != a.ef);
+                !(a.do_rerank && a.depth != a.ef) && !a.relax;
     if (coop) coop = coop_env > 0 ? nq <= (uint64_t)coop_env : nq <= pinfo.coop_cap;
     if (pipelined) {
         // The chunk copies are submitted BEFORE the search launch: in normal

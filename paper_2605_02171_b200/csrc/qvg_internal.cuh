@@ -69,10 +69,11 @@ struct qvg_index {
     bool has_tmap = false;
     // launch plans keyed by (ef, tie capacity, visited-slot request, extra depth)
     struct PlanKey {
-        uint32_t ef, tcap, vreq, xa;
+        uint32_t ef, tcap, vreq, xa, relax;
         bool operator<(const PlanKey& o) const {
             if (ef != o.ef) return ef < o.ef;
             if (tcap != o.tcap) return tcap < o.tcap;
+            if (relax != o.relax) return relax < o.relax;
             return vreq != o.vreq ? vreq < o.vreq : xa < o.xa;
         }
     };
@@ -124,6 +125,7 @@ struct SearchLaunch {
                             // reranked; depth == ef is the reference (search.cpp:138)
     const uint32_t* ready;  // nullable: queries [0, *ready) have landed in qraw
                             // (pipelined upload; the warp waits before its prologue)
+    uint32_t relax;         // 0: exact search; 2 / 4: relaxed variant, expansions per step
 };
 
 // keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)
@@ -134,7 +136,10 @@ __host__ __device__ inline uint32_t extra_depth(uint32_t ef, uint32_t depth) { r
 // default visited-table size (log2 slots): the largest table (256..4096
 // slots, >= ef) among those that keep the maximum number of resident blocks
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
-                           uint32_t xa = 0);
+                           uint32_t xa = 0, uint32_t relax = 0);
+// per-lane row-slot capacity of the relaxed search kernel for max degree R and
+// `relax` expansions per step (0 = geometry not supported)
+uint32_t relaxed_rw(uint32_t R, uint32_t relax);
 // contiguous bytes of the search kernel's per-warp TMA stage (both halves)
 uint32_t search_stage_bytes(const DevIndex& ix);
 

@@ -158,12 +158,13 @@ __host__ __device__ inline uint32_t stage_rows_for(uint32_t W, uint32_t RM, uint
 // register budget per template: enough blocks that shared memory, not
 // registers, bounds residency at the BASELINE geometries (R=32 rows -> ~9
 // blocks of 2 warps fit in smem; R=64 -> ~7)
-template <int RW>
+template <int RW, int RELP = 0>
 #ifndef QVG_MINBLOCKS_RW2
 #define QVG_MINBLOCKS_RW2 7
 #endif
 struct MinBlocks {
-    static constexpr int value = RW == 1 ? 9 : (RW == 2 ? QVG_MINBLOCKS_RW2 : 5);
+    static constexpr int value =
+        RELP ? (RW <= 2 ? 8 : 6) : (RW == 1 ? 9 : (RW == 2 ? QVG_MINBLOCKS_RW2 : 5));
 };
 
 // XA: rerank deeper than ef.  A = the best `xa` scored keys outside P, kept
@@ -175,13 +176,22 @@ struct MinBlocks {
 // SPLIT: several lanes per scored row (wide rows, few rows per stage half); a
 // separate instantiation because the extra loop costs the narrow-row kernels
 // ~1.5% even when unused (cfg2 A/B, tools/tune_search.py).
-template <int RW, bool XA, bool SPLIT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
+// RELP > 0: the RELAXED variant (reported separately,
+// never used for parity): each step expands the RELP best unexpanded pool
+// entries at once and scores the union of their neighbours, admission is
+// merge-then-truncate (no prefix rule) and there is no tie stack — fewer,
+// wider serial steps per query.  RW is then the capacity of RELP rows, each
+// lane holding RW / RELP slots of every picked row.
+template <int RW, bool XA, bool SPLIT, int RELP = 0>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
                   const int use_tmap, const uint32_t SL) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr uint32_t RM = RW * 32;
+    constexpr bool REL = RELP > 0;
+    constexpr int SPL = REL ? RW / RELP : RW;  // adjacency slots per lane per picked row
+    static_assert(!REL || (SPL >= 1 && SPL * RELP == RW && !XA), "relaxed geometry");
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -410,7 +420,51 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
         __syncwarp();
         uint32_t spec_u = kSentinel;  // speculatively prefetched adjacency row
         uint64_t spec_key = kInfKey;  // its key (the predicted next pick)
+        uint32_t spec_rel[REL ? RELP : 1];  // relaxed: the predicted picks, spec_n of them
+        uint32_t spec_n = 0;
+        (void)spec_rel;
+        (void)spec_n;
         uint32_t spec_v[RW];
+        // relaxed: the first (up to RELP) unexpanded pool entries at/after the
+        // hint, in key order -> ids[], count returned; mark = set their EXP bit
+        auto first_unexpanded = [&](uint32_t* ids, bool mark, uint32_t& last) -> uint32_t {
+            uint32_t cnt = 0;
+            for (uint32_t b0 = hint & ~31u; b0 < np && cnt < (uint32_t)RELP; b0 += 32) {
+                const uint32_t idx = b0 + lane;
+                const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
+                unsigned bal = __ballot_sync(kFull, un);
+                while (bal && cnt < (uint32_t)RELP) {
+                    const uint32_t at = b0 + __ffs(bal) - 1;
+                    const uint32_t id = (uint32_t)pk[at];
+#pragma unroll
+                    for (int t = 0; t < (REL ? RELP : 1); ++t)
+                        if ((uint32_t)t == cnt) ids[t] = id;
+                    if (mark && lane == 0) pk[at] |= kExp;
+                    last = at;
+                    ++cnt;
+                    bal &= bal - 1;
+                }
+            }
+            return cnt;
+        };
+        // relaxed: slots of picked row p -> v[p*SPL, (p+1)*SPL)
+        auto load_rows = [&](uint32_t* vv, const uint32_t* ids, uint32_t cnt) {
+#pragma unroll
+            for (int p = 0; p < (REL ? RELP : 1); ++p) {
+                const bool have = (uint32_t)p < cnt && lane * SPL < ix.RS;
+                const uint32_t* row = ix.adj + (size_t)(have ? ids[p] : 0u) * ix.RS;
+                if (SPL == 1) {
+                    vv[p * SPL] = have ? __ldg(row + lane) : kSentinel;
+                } else {
+                    const uint2 t = have ? __ldg(reinterpret_cast<const uint2*>(row) + lane)
+                                         : make_uint2(kSentinel, kSentinel);
+                    vv[p * SPL] = t.x;
+                    vv[p * SPL + SPL - 1] = t.y;
+                }
+            }
+        };
+        (void)first_unexpanded;
+        (void)load_rows;
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
         QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0, ph_tma = 0;)
@@ -424,7 +478,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             QVG_PH(ph_tma += clock64() - tp0;)
             // speculative prefetch: adjacency row of the current best unexpanded
             // entry (the next pick unless this row inserts a better one)
-            {
+            if constexpr (REL) {
+                uint32_t last = 0;
+                spec_n = first_unexpanded(spec_rel, false, last);
+                load_rows(spec_v, spec_rel, spec_n);
+            } else {
                 uint32_t guess = kSentinel;
                 spec_key = kInfKey;
                 for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
@@ -485,7 +543,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     crp[pos] = rp;
                 }
                 m += __popc(bal);
-                if (ctd_prefetch && bal) {
+                if (ctd_prefetch && !REL && bal) {
                     // the smallest contender is always admitted (no smaller
                     // earlier contender, and it beats max(P)); if it also beats
                     // the predicted pick it becomes the next pick: fetch its
@@ -630,6 +688,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             // (L2 prefetch of the predicted next pick's neighbour rows here was
             // measured: TMA bulk prefetch +25% time, LSU line prefetch +0.7%)
 
+            if constexpr (REL) {
+                // relaxed: a node reached through two picked rows (past a lossy
+                // visited-table collision) can be a contender twice; keep the
+                // first copy (later copies become +inf and sort past the rest)
+                if (m > 1) {
+                    bool dup[RW];
+#pragma unroll
+                    for (int i = 0; i < RW; ++i) dup[i] = false;
+                    uint64_t yv[RW];
+#pragma unroll
+                    for (int i = 0; i < RW; ++i) yv[i] = lane + 32u * i < m ? ctd[lane + 32u * i] : kInfKey;
+                    for (uint32_t j = 0; j < m; ++j) {
+                        const uint64_t yj = ctd[j];
+#pragma unroll
+                        for (int i = 0; i < RW; ++i) dup[i] |= (yj == yv[i]) & (j < lane + 32u * i);
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < RW; ++i)
+                        if (dup[i] && lane + 32u * i < m) ctd[lane + 32u * i] = kInfKey;
+                    __syncwarp();
+                }
+            }
             if (m > 0) {
                 // (c) contender ranks (key order) and prefix counts (row order)
                 uint64_t y[RW];
@@ -651,16 +732,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                         pre[i] += lt & (j < lane + 32u * i);
                     }
                 }
+                uint32_t mu = m;  // distinct contenders (relaxed: duplicates are +inf)
+                if constexpr (REL) {
+                    uint32_t fin = 0;
+#pragma unroll
+                    for (int i = 0; i < RW; ++i)
+                        fin += __popc(__ballot_sync(kFull, lane + 32u * i < m && y[i] != kInfKey));
+                    mu = fin;
+                }
 #pragma unroll
                 for (int i = 0; i < RW; ++i)
-                    if (lane + 32u * i < m) csrp[rk[i]] = rp[i];
+                    if (lane + 32u * i < m && (!REL || y[i] != kInfKey)) csrp[rk[i]] = rp[i];
                 __syncwarp();
 
                 // (d) in-place merge: P entries at index >= lo shift right by
                 // #{contenders with rank-in-P <= index}; walk chunks backwards so
                 // no entry is overwritten before it is read
-                const uint32_t lo = csrp[0];
-                const uint32_t total = np + m;
+                const uint32_t lo = mu ? csrp[0] : np;
+                const uint32_t total = np + mu;
                 if (lo < np) {
                     for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
                         const uint32_t idx = (uint32_t)cb + lane;
@@ -669,29 +758,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                         uint32_t npos = 0;
                         if (mv) {
                             p = pk[idx];
-                            npos = idx + upper_bound_u32(csrp, m, idx);
+                            npos = idx + upper_bound_u32(csrp, mu, idx);
                         }
                         __syncwarp();
                         if (mv) {
                             if (npos < ef) pk[npos] = p;
-                            else evk[npos - ef] = p;  // exp bit set = not a tie candidate
+                            else if (!REL) evk[npos - ef] = p;  // exp bit set = not a tie candidate
                         }
                         __syncwarp();
                     }
                 }
 #pragma unroll
                 for (int i = 0; i < RW; ++i) {
-                    if (lane + 32u * i < m) {
+                    if (lane + 32u * i < m && (!REL || y[i] != kInfKey)) {
                         const uint32_t npos = rk[i] + rp[i];
                         if (npos < ef) pk[npos] = y[i];
-                        else evk[npos - ef] = (rp[i] + pre[i]) < ef ? y[i] : (y[i] | kExp);
+                        else if (!REL) evk[npos - ef] = (rp[i] + pre[i]) < ef ? y[i] : (y[i] | kExp);
                     }
                 }
                 __syncwarp();
                 if (lo < hint) hint = lo;
 
-                // (e) tie stack maintenance
-                if (total > ef) {
+                // (e) tie stack maintenance (none in the relaxed variant)
+                if (!REL && total > ef) {
                     const uint32_t wd = kdist(pk[ef - 1]);
                     if (tn == 0 || wd < tdist) {
                         tn = 0;
@@ -773,7 +862,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             // worst(P).dist, so the reference's stop test, search.cpp:48, does
             // not fire for it)
             uint32_t u = kSentinel;
-            for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
+            uint32_t v[RW];
+            if constexpr (REL) {
+                // relaxed: take the first RELP unexpanded entries; stop when none
+                uint32_t picks[RELP], last = 0;
+                const uint32_t cnt = first_unexpanded(picks, true, last);
+                if (cnt == 0) break;
+                hint = last + 1;
+                c_exp += cnt;
+                bool same = cnt == spec_n;
+#pragma unroll
+                for (int t = 0; t < RELP; ++t) same &= (uint32_t)t >= cnt || picks[t] == spec_rel[t];
+                if (same) {
+#pragma unroll
+                    for (int j = 0; j < RW; ++j) v[j] = spec_v[j];
+                } else {
+                    load_rows(v, picks, cnt);
+                }
+                __syncwarp();  // EXP marks visible before the next scan
+            }
+            for (uint32_t b0 = hint & ~31u; !REL && b0 < np; b0 += 32) {
                 const uint32_t idx = b0 + lane;
                 const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
                 const unsigned bal = __ballot_sync(kFull, un);
@@ -786,19 +894,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
                     break;
                 }
             }
-            if (u == kSentinel) {
+            if (!REL && u == kSentinel) {
                 hint = np;
                 if (tn == 0) break;
                 u = tie[tn - 1];
                 --tn;
                 ++c_tie;
             }
-            ++c_exp;
+            if (!REL) ++c_exp;
 
             // (g) adjacency row (stored order): the speculative prefetch when it
             // guessed right, else a fresh vectorised load
-            uint32_t v[RW];
-            if (u == spec_u) {
+            if (REL) {
+                // loaded above
+            } else if (u == spec_u) {
 #pragma unroll
                 for (int j = 0; j < RW; ++j) v[j] = spec_v[j];
             } else {
@@ -827,6 +936,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW>::value)
             bool keep[RW];
 #pragma unroll
             for (int j = 0; j < RW; ++j) {
+                if (REL && j > 0 && j % SPL == 0) __syncwarp();  // next picked row sees this one's marks
                 const uint32_t id = v[j];
                 bool k2 = id != kSentinel;
                 if (k2) {
@@ -1086,13 +1196,35 @@ void* pick_kernel(bool xa, bool split) {
     return split ? (void*)search_kernel<RW, false, true> : (void*)search_kernel<RW, false, false>;
 }
 
+// relaxed variant: RW = capacity of `relax` picked rows
+void* pick_relaxed(uint32_t rw, uint32_t relax, bool split) {
+    if (relax == 2 && rw == 2) return split ? (void*)search_kernel<2, false, true, 2> : (void*)search_kernel<2, false, false, 2>;
+    if (relax == 2 && rw == 4) return split ? (void*)search_kernel<4, false, true, 2> : (void*)search_kernel<4, false, false, 2>;
+    if (relax == 4 && rw == 4) return split ? (void*)search_kernel<4, false, true, 4> : (void*)search_kernel<4, false, false, 4>;
+    return nullptr;
+}
+
+}  // namespace
+
+// row-slot capacity per lane of the relaxed variant (0 = unsupported geometry)
+uint32_t relaxed_rw(uint32_t R, uint32_t relax) {
+    const uint32_t per = (R + 31) / 32;  // slots per lane of one row
+    if (relax == 2 && per == 1) return 2;
+    if (relax == 2 && per == 2) return 4;
+    if (relax == 4 && per == 1) return 4;
+    return 0;
+}
+
+namespace {
+
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap,
-               uint32_t xa) {
+               uint32_t xa, uint32_t relax = 0) {
     Plan p;
-    p.rw = pow2ceil((ix.R + 31) / 32);
+    p.rw = relax ? relaxed_rw(ix.R, relax) : pow2ceil((ix.R + 31) / 32);
     p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
-    if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
+    if (relax) p.fn = pick_relaxed(p.rw, relax, split);
+    else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
@@ -1162,13 +1294,13 @@ uint32_t search_stage_bytes(const DevIndex& ix) {
 }
 
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
-                           uint32_t xa) {
+                           uint32_t xa, uint32_t relax) {
     uint32_t min_log = 8;  // 256 slots
     while ((1u << min_log) < ((ef + xa + 31u) & ~31u)) ++min_log;  // rerank scores alias it
     uint32_t best_log = min_log;
     int best_blocks = -1;
     for (uint32_t lg = min_log; lg <= 12 || lg == min_log; ++lg) {
-        const Plan p = make_plan(ix, ef, lg, tie_cap, xa);
+        const Plan p = make_plan(ix, ef, lg, tie_cap, xa, relax);
         if (p.block_bytes > max_dyn_smem(device) || !allow_max_smem(p.fn, device)) {
             break;
         }
@@ -1193,7 +1325,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         set_error("search: visited_slots must be >= ef + extra rerank depth (rounded to 32)");
         return QVG_INVALID_ARGUMENT;
     }
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa);
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa, a.relax);
     if (p.block_bytes > max_dyn_smem(device)) {
         set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
         return QVG_INVALID_ARGUMENT;
@@ -1225,7 +1357,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
 
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s) {
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth));
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth), a.relax);
     alignas(64) CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
     const CUtensorMap* m = tmap ? tmap : &dummy;

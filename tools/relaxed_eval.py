@@ -1,0 +1,89 @@
+"""Relaxed variant vs the exact search on a config graph.
+
+    python tools/relaxed_eval.py CONFIG [SIGMA_MODE] [EFS]
+
+Per ef and relax in {0 (exact), 2, 4 (R <= 32 only)}: kernel ms (20 launches
+after 3 warm-ups, L2 flushed before each), QPS, Recall@10 against exact float
+ground truth on the first 1000 queries, expansions and evals per query, and
+structural checks (unique ids, sorted pool).  The exact rows also check ids
+against an exact-visited pass.
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2605_02171_b200 as Q  # noqa: E402
+from paper_2605_02171_b200 import _native as N, datasets, graphs  # noqa: E402
+
+cfgn = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+mode = sys.argv[2] if len(sys.argv) > 2 else "literal"
+efs = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [16, 32, 64, 128]
+cfg = datasets.CONFIGS[cfgn]
+base, queries = datasets.config_data(cfg, nq=10000, sigma_mode=mode)
+g = graphs.load_graph(cfg, mode, base.shape[0], base)
+if g is None:
+    g = graphs.load_graph(cfg, mode, base.shape[0], base, builder="gpu")
+qn, codes, _ = Q.encode_queries(base)
+ix = Q.GpuIndex.from_arrays(codes, g["adj"], qn, int(g["entry"]))
+R = g["adj"].shape[1] - 1
+base_dev = torch.from_numpy(qn).cuda()
+del codes
+rq = 1000
+qnq, _, _ = Q.encode_queries(queries[:rq])
+gt = Q.brute_force_topk(base_dev, torch.from_numpy(qnq).cuda(), 10)
+del base_dev, qn
+nq = len(queries)
+q = torch.from_numpy(queries).cuda()
+ids = torch.empty((nq, 10), dtype=torch.int32, device="cuda")
+sc = torch.empty((nq, 10), dtype=torch.float32, device="cuda")
+cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+stt = torch.empty(nq, dtype=torch.int32, device="cuda")
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+ix.set_stream(torch.cuda.current_stream())
+
+
+def recall(res):
+    return float(np.mean([len(set(r[:10].tolist()) & set(t[:10].tolist())) / 10
+                          for r, t in zip(res[:rq], gt)]))
+
+
+out = []
+for ef in efs:
+    for relax in (0, 2, 4):
+        if relax == 4 and R > 32:
+            continue
+        r = ix.search_ex(queries, k=10, ef=ef, relaxed=relax)
+        assert (r["status"] == 0).all()
+        pid = r["pool_ids"].astype(np.int64)
+        pdist = r["pool_dists"].astype(np.int64)
+        keys = (pdist << 32) | pid
+        ok_sorted = bool((np.diff(keys, axis=1) > 0).all())
+        ok_unique = all(len(set(x.tolist())) == 10 for x in r["ids"])
+        opts = N.qvg_search_opts(entry_point=N.SENTINEL, timing_only=1, relaxed_expansions=relax)
+        ks = []
+        for it in range(23):
+            flush.zero_()
+            st = N.qvg_stats()
+            rc = N.lib().qvg_search_ex(ix._h, q.data_ptr(), nq, 10, ef, C.byref(opts),
+                                       ids.data_ptr(), sc.data_ptr(), cnt.data_ptr(),
+                                       stt.data_ptr(), None, None, None, None, C.byref(st))
+            assert rc == 0, N.last_error()
+            if it >= 3:
+                ks.append(st.search_ms)
+        ks.sort()
+        row = dict(ef=ef, relax=relax, kernel_ms=ks[len(ks) // 2], qps=nq / ks[len(ks) // 2] * 1e3,
+                   recall_at_10=recall(r["ids"]),
+                   expansions=r["stats"]["expansions"] / nq, evals=r["stats"]["dist_evals"] / nq,
+                   sorted=ok_sorted, unique=ok_unique)
+        if relax == 0:
+            ex = ix.search_ex(queries, k=10, ef=ef, exact_visited=True, pools=False)
+            row["same_as_exact_visited"] = bool((ex["ids"] == r["ids"]).all())
+        out.append(row)
+        print(json.dumps(row), flush=True)
