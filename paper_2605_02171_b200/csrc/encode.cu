@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128) encode_tiled_kernel(
     }
 }
 
-// Lane-per-query (default): a block of 128 threads owns QB <= 32 consecutive
+// Lane-per-query (default): a block of 512 threads owns QB <= 32 consecutive
 // queries staged in shared memory with an odd row stride ld (at step i lane q
 // reads word q*ld + i: 32 distinct banks).  Lane q of warp 0 runs query q's two
 // index-ordered double reductions, so one FP64 warp-instruction advances 32
@@ -133,8 +133,9 @@ __global__ void __launch_bounds__(128) encode_tiled_kernel(
 // B200 whatever the active-lane count (tools/fp64_chain_bench.cu), so a lane-0
 // chain per query leaves 31/32 of it idle and throughput-bound.  Staging,
 // scaling, the qn stores and the bit packing (two ballots per 32 elements) are
-// element-parallel over the block's four warps.
-constexpr uint32_t kLpqThreads = 128;
+// element-parallel over the block's 16 warps (staging is load-latency bound:
+// more warps keep more row loads in flight).
+constexpr uint32_t kLpqThreads = 512;  // 16 warps stage the rows (loads in flight); warp 0 chains
 
 __device__ __forceinline__ uint32_t lpq_ld(uint32_t dim) { return dim | 1u; }
 
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kLpqThreads) encode_lpq_kernel(
     const uint64_t q0 = (uint64_t)blockIdx.x * QB;
     const uint32_t nb = (uint32_t)min((uint64_t)QB, nq - q0);
     const uint32_t ld = lpq_ld(dim);
+    const bool vec4 = (dim & 3u) == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
     if (tid < 32) s_bad[tid] = s_ybad[tid] = 0;
     __syncthreads();
     // stage the rows (warp per row, coalesced) + finite check (search.cpp:128-131)
@@ -157,11 +159,24 @@ __global__ void __launch_bounds__(kLpqThreads) encode_lpq_kernel(
         const float* src = x + (q0 + r) * dim;
         float* row = rows + (size_t)r * ld;
         bool bad = false;
-#pragma unroll 4
-        for (uint32_t i = lane; i < dim; i += 32) {
-            const float v = __ldg(src + i);
-            bad |= !isfinite(v);
-            row[i] = v;
+        if (vec4) {
+            const float4* src4 = reinterpret_cast<const float4*>(src);
+#pragma unroll 6
+            for (uint32_t i = lane; i < dim / 4; i += 32) {
+                const float4 v = __ldg(src4 + i);
+                bad |= !(isfinite(v.x) & isfinite(v.y) & isfinite(v.z) & isfinite(v.w));
+                row[4 * i] = v.x;
+                row[4 * i + 1] = v.y;
+                row[4 * i + 2] = v.z;
+                row[4 * i + 3] = v.w;
+            }
+        } else {
+#pragma unroll 8
+            for (uint32_t i = lane; i < dim; i += 32) {
+                const float v = __ldg(src + i);
+                bad |= !isfinite(v);
+                row[i] = v;
+            }
         }
         bad = __any_sync(0xFFFFFFFFu, bad);
         if (lane == 0 && bad) s_bad[r] = 1;
@@ -501,7 +516,7 @@ void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float
         for (uint32_t c = 32; c >= 4; --c) {
             const size_t sm = row_bytes * c;
             if (sm > cap) continue;
-            const uint64_t per_sm = std::min<uint64_t>(227u * 1024u / (sm + 1024u), 16u);
+            const uint64_t per_sm = std::min<uint64_t>(227u * 1024u / (sm + 1024u), 2048u / kLpqThreads);
             if (!qb) qb = c;  // largest that fits in shared memory
             if ((nq + c - 1) / c <= per_sm * (uint64_t)sms) {
                 qb = c;
