@@ -182,7 +182,10 @@ struct MinBlocks {
 // merge-then-truncate (no prefix rule) and there is no tie stack — fewer,
 // wider serial steps per query.  RW is then the capacity of RELP rows, each
 // lane holding RW / RELP slots of every picked row.
-template <int RW, bool XA, bool SPLIT, int RELP = 0>
+// WC > 0: the code width W as a compile-time constant (the headline geometry
+// W = 12 has its own instantiation: constant row/group strides, fully
+// unrolled distance loop).
+template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     const DevIndex ix = a.ix;
-    const uint32_t W = ix.W;
+    const uint32_t W = WC ? (uint32_t)WC : ix.W;
     const uint32_t rowb = 16u * W;
     const uint32_t gstride = group_stride(W);  // bytes per 4-row TMA group (128-B aligned)
     const uint32_t VS = 1u << a.vis_log2;
@@ -657,12 +660,30 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                     if (valid) {
                         const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
                         // (row_sm2 here measured 0.8 % slower at W = 12)
-                        uint32_t cc = rot;
                         Sm2Acc acc;
+                        if constexpr (WC > 0 && ((16 * WC) & 127) == 64) {
+                            // rows 64 B past a 128-B boundary: a rotation by
+                            // (lane >> 1) & 3 puts an 8-lane LDS.128 phase on 8
+                            // distinct bank quads and lets the first W - 3 chunks
+                            // use constant offsets (no wrap)
+                            const uint32_t r4 = (lane >> 1) & 3u;
+                            const uint4* qr = qc + r4;
+                            const uint4* rr = rowp + r4;
+#pragma unroll
+                            for (int c = 0; c < WC - 3; ++c) acc.add(qr[c], rr[c]);
+#pragma unroll
+                            for (int c = WC - 3; c < WC; ++c) {
+                                uint32_t cc = (uint32_t)c + r4;
+                                cc = cc >= (uint32_t)WC ? cc - WC : cc;
+                                acc.add(qc[cc], rowp[cc]);
+                            }
+                        } else {
+                            uint32_t cc = rot;
 #pragma unroll 4
-                        for (uint32_t c = 0; c < W; ++c) {
-                            acc.add(qc[cc], rowp[cc]);
-                            cc = cc + 1u == W ? 0u : cc + 1u;
+                            for (uint32_t c = 0; c < W; ++c) {
+                                acc.add(qc[cc], rowp[cc]);
+                                cc = cc + 1u == W ? 0u : cc + 1u;
+                            }
                         }
                         d = acc.total();
                     }
@@ -1225,6 +1246,12 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
+    else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
+#ifndef QVG_NO_WC_EXTRA
+    else if (p.rw == 1 && !xa && !split && ix.W == 6) p.fn = (void*)search_kernel<1, false, false, 0, 6>;
+    else if (p.rw == 2 && !xa && split && ix.W == 24) p.fn = (void*)search_kernel<2, false, true, 0, 24>;
+    else if (p.rw == 2 && !xa && split && ix.W == 48) p.fn = (void*)search_kernel<2, false, true, 0, 48>;
+#endif
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,

@@ -470,3 +470,26 @@ def test_relaxed_variant_recall_within_half_point():
         for relax in (2, 4):
             rel = recall(ix.search_ex(q, k=10, ef=ef, relaxed=relax, pools=False)["ids"])
             assert rel >= exact - 0.005, (ef, relax, exact, rel)
+
+
+@pytest.mark.gpu
+@ref_only
+@pytest.mark.parametrize("dim,m", [(768, 32), (384, 16)])
+def test_headline_code_width_parity_vs_reference(dim, m):
+    """The compile-time code-width instantiations (W = 12 at D = 768, the
+    headline geometry; W = 6 at D = 384) against the reference's own
+    run_query_batch on a reference-built graph: bit-identical ids and scores,
+    identical pools vs the dual-heap oracle."""
+    from paper_2605_02171_b200.datasets import mixture
+    base, q = mixture(8_000, dim, 100, 0.3, seed=5, nq=400, sigma_mode="norm")
+    ref = O.RefIndex.build(base, m=m, ef_c=64, alpha=1.2, threads=os.cpu_count())
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    orc = O.OracleIndex.from_ref(ref)
+    for ef in (16, 64, 128):
+        ids, sc, cnt = ref.run_query_batch(q, ef, 10, threads=os.cpu_count())
+        r = ix.search_ex(q, k=10, ef=ef)
+        assert np.array_equal(r["ids"], ids), ef
+        assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32)), ef
+        o = orc.query_batch(q, ef, 10, mode=0, pools=True)
+        assert np.array_equal(r["pool_ids"], o["pool_ids"]), ef
+        assert np.array_equal(r["pool_dists"], o["pool_dists"]), ef
