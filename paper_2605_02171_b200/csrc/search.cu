@@ -185,11 +185,15 @@ struct MinBlocks {
 // WC > 0: the code width W as a compile-time constant (the headline geometry
 // W = 12 has its own instantiation: constant row/group strides, fully
 // unrolled distance loop).
-template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0>
+// GEO: also the default stage geometry as constants (32 rows per stage half,
+// 48-float rerank slices), dispatched when the launch uses exactly those.
+template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
-                  const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR,
-                  const int use_tmap, const uint32_t SL) {
+                  const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
+                  const int use_tmap, const uint32_t SL_in) {
+    const uint32_t SR = GEO ? 32u : SR_in;
+    const uint32_t SL = (GEO && SL_in) ? 48u : SL_in;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr uint32_t RM = RW * 32;
     constexpr bool REL = RELP > 0;
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     const uint32_t rowb = 16u * W;
     const uint32_t gstride = group_stride(W);  // bytes per 4-row TMA group (128-B aligned)
     const uint32_t VS = 1u << a.vis_log2;
-    const uint32_t ef = a.ef;
+    const uint32_t ef = a.ef;  // (a compile-time ef = 64 instantiation measured +0.3 %)
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
     const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa);
@@ -1246,6 +1250,8 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
+    else if (p.rw == 2 && !xa && !split && ix.W == 12 && p.SR == 32 && stage_half_bytes() == 6144)
+        p.fn = (void*)search_kernel<2, false, false, 0, 12, true>;
     else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
 #ifndef QVG_NO_WC_EXTRA
     else if (p.rw == 1 && !xa && !split && ix.W == 6) p.fn = (void*)search_kernel<1, false, false, 0, 6>;
