@@ -49,4 +49,7 @@ print(f"  query time us: mean {(end - start).mean() / 1e3:.1f} p50 {np.median(en
 for frac in (0.9, 0.5, 0.1):
     below = (active < frac * slots).mean()
     print(f"  span fraction with < {int(frac * 100)}% of warp slots busy: {below:.3f}")
+np.savez(os.path.join(ROOT, "gpurun_out", f"tail_cfg{cfg.name}_ef{ef}.npz"), start=start, end=end,
+         warp=warp, counters_exp=ix.search_ex(qd, k=10, ef=ef, pools=False)["counters"][:, 0],
+         pool0=ix.search_ex(qd, k=10, ef=ef)["pool_dists"][:, 0])
 print(f"  first time below 90 pct busy: {ts[np.argmax(active < 0.9 * slots)] / 1e3:.1f} us")
