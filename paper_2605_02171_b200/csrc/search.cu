@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         __syncwarp();
         uint32_t spec_u = kSentinel;  // speculatively prefetched adjacency row
         uint64_t spec_key = kInfKey;  // its key (the predicted next pick)
+        uint32_t guess_idx = kSentinel;  // its index in P (kSentinel: not in P)
         uint32_t spec_rel[REL ? RELP : 1];  // relaxed: the predicted picks, spec_n of them
         uint32_t spec_n = 0;
         (void)spec_rel;
@@ -492,12 +493,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             } else {
                 uint32_t guess = kSentinel;
                 spec_key = kInfKey;
+                guess_idx = kSentinel;
                 for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
                     const uint32_t idx = b0 + lane;
                     const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
                     const unsigned bal = __ballot_sync(kFull, un);
                     if (bal) {
-                        spec_key = ordk(pk[b0 + __ffs(bal) - 1]);
+                        guess_idx = b0 + __ffs(bal) - 1;
+                        spec_key = ordk(pk[guess_idx]);
                         guess = (uint32_t)spec_key;
                         break;
                     }
@@ -736,6 +739,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                     __syncwarp();
                 }
             }
+            uint32_t ins_lo = kSentinel;  // P index of this step's smallest contender
             if (m > 0) {
                 // (c) contender ranks (key order) and prefix counts (row order)
                 uint64_t y[RW];
@@ -774,6 +778,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 // #{contenders with rank-in-P <= index}; walk chunks backwards so
                 // no entry is overwritten before it is read
                 const uint32_t lo = mu ? csrp[0] : np;
+                ins_lo = lo;
                 const uint32_t total = np + mu;
                 if (lo < np) {
                     for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
@@ -906,17 +911,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 }
                 __syncwarp();  // EXP marks visible before the next scan
             }
-            for (uint32_t b0 = hint & ~31u; !REL && b0 < np; b0 += 32) {
-                const uint32_t idx = b0 + lane;
-                const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
-                const unsigned bal = __ballot_sync(kFull, un);
-                if (bal) {
-                    const uint32_t pick = b0 + __ffs(bal) - 1;
+            // No scan: entries of P before this step's first insertion point
+            // are unchanged, so the first unexpanded entry at/after the hint is
+            // the predicted pick (first unexpanded after the last pick, found by
+            // the speculative scan) unless the smallest new contender — always
+            // admitted, at index ins_lo — comes first.
+            if (!REL) {
+                const uint32_t pick = ins_lo < guess_idx ? ins_lo : guess_idx;
+                if (pick != kSentinel) {
                     u = (uint32_t)pk[pick];
                     __syncwarp();
                     if (lane == 0) pk[pick] |= kExp;
                     hint = pick + 1;
-                    break;
                 }
             }
             if (!REL && u == kSentinel) {
