@@ -422,6 +422,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         uint32_t na = 0;  // |A| (XA only)
         uint32_t c_exp = 0, c_tie = 0, c_eval = 0, c_drop = 0, c_slots = 0, c_maxtie = 0;
         bool overflow = false;
+#ifdef QVG_TAIL
+        uint32_t c_mtot = 0;  // contenders per query (diagnostics)
+#endif
         uint32_t n = 1;  // rows to score in cid[0..n)
         if (lane == 0) cid[0] = entry;
         __syncwarp();
@@ -740,6 +743,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 }
             }
             uint32_t ins_lo = kSentinel;  // P index of this step's smallest contender
+#ifdef QVG_TAIL
+            c_mtot += m;
+#endif
             if (m > 0) {
                 // (c) contender ranks (key order) and prefix counts (row order)
                 uint64_t y[RW];
@@ -1171,6 +1177,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             a.qctr[q * 8 + 1] = (uint32_t)tg1;
             a.qctr[q * 8 + 2] = (uint32_t)gwarp;
             a.qctr[q * 8 + 3] = blockIdx.x;
+            a.qctr[q * 8 + 4] = c_mtot;
         }
 #endif
         __syncwarp();
