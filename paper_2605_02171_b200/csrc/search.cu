@@ -262,11 +262,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         __syncwarp();
         for (uint32_t g = lane; g < ng; g += 32) {
             if (use_tmap) {
-                const uint32_t j = r0 + 4u * g;
-                const uint32_t i0 = cid[j];
-                const uint32_t i1 = 4u * g + 1u < cnt ? cid[j + 1] : i0;
-                const uint32_t i2 = 4u * g + 2u < cnt ? cid[j + 2] : i0;
-                const uint32_t i3 = 4u * g + 3u < cnt ? cid[j + 3] : i0;
+                const uint32_t j = r0 + 4u * g;  // multiple of 4: one 16-B load
+                const uint4 c4 = *reinterpret_cast<const uint4*>(cid + j);
+                const uint32_t i0 = c4.x;
+                const uint32_t i1 = 4u * g + 1u < cnt ? c4.y : i0;
+                const uint32_t i2 = 4u * g + 2u < cnt ? c4.z : i0;
+                const uint32_t i3 = 4u * g + 3u < cnt ? c4.w : i0;
                 tma_gather4(stage0 + h * stage_delta + (size_t)g * gstride, &tmap, i0, i1, i2, i3, bar);
             } else {
                 bulk_row(stage0 + h * stage_delta + (size_t)(g >> 2) * gstride + (g & 3u) * rowb, ix.codes + (size_t)cid[r0 + g] * W, rowb,
