@@ -52,6 +52,5 @@ for frac in (0.9, 0.5, 0.1):
 np.savez(os.path.join(ROOT, "gpurun_out", f"tail_cfg{cfg.name}_ef{ef}.npz"), start=start, end=end,
          warp=warp, counters_exp=ix.search_ex(qd, k=10, ef=ef, pools=False)["counters"][:, 0],
          pool0=ix.search_ex(qd, k=10, ef=ef)["pool_dists"][:, 0])
-nexp = ix.search_ex(qd, k=10, ef=ef, pools=False, exact_visited=True)["stats"]["expansions"] / len(c)
-print(f"  contenders per query {c[:, 4].mean():.1f} (per expansion {c[:, 4].mean() / nexp:.2f})")
+print(f"  contenders per query {c[:, 4].mean():.1f}")
 print(f"  first time below 90 pct busy: {ts[np.argmax(active < 0.9 * slots)] / 1e3:.1f} us")
