@@ -926,9 +926,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             if (!REL) {
                 const uint32_t pick = ins_lo < guess_idx ? ins_lo : guess_idx;
                 if (pick != kSentinel) {
-                    u = (uint32_t)pk[pick];
+                    // spec_key already is this entry's key: the speculative scan
+                    // set it to the predicted pick and the contender prefetch
+                    // lowered it to the smallest admitted contender if smaller
+                    u = (uint32_t)spec_key;
                     __syncwarp();
-                    if (lane == 0) pk[pick] |= kExp;
+                    if (lane == 0) pk[pick] = spec_key | kExp;
                     hint = pick + 1;
                 }
             }
