@@ -1058,7 +1058,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 // into a stage half; lane r owns row 32g + r and advances its 4
                 // chains slice by slice, i.e. in ascending element order, which
                 // keeps every chain's rounding sequence identical to dot_f32.
-                const uint32_t dim = ix.dim;
+                const uint32_t dim = GEO ? 768u : ix.dim;  // GEO is dispatched for D = 768 only
                 const uint32_t main4 = dim & ~3u;
                 const uint32_t nsl = (dim + SL - 1) / SL;
                 const uint32_t nsl_m = 0xFFFFFFFFu / nsl + 1u;  // t / nsl == __umulhi(t, nsl_m)
@@ -1267,7 +1267,8 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
-    else if (p.rw == 2 && !xa && !split && ix.W == 12 && p.SR == 32 && stage_half_bytes() == 6144)
+    else if (p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
+             stage_half_bytes() == 6144)
         p.fn = (void*)search_kernel<2, false, false, 0, 12, true>;
     else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
 #ifndef QVG_NO_WC_EXTRA
