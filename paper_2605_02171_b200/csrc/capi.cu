@@ -305,7 +305,11 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         const char* v = getenv("QVG_PIPELINE");
         return !(v && v[0] == '0');
     }();
-    constexpr uint64_t kChunk = 1024;
+    static const uint64_t kChunk = [] {  // queries per pipelined upload chunk
+        const char* v = getenv("QVG_CHUNK");
+        const long long c = v ? atoll(v) : 1024;
+        return (uint64_t)(c < 32 ? 32 : c);
+    }();
     const bool stage_ok = 4ull * ix.dim <= search_stage_bytes(ix);
     const bool pipelined = mode.encode && !in_dev && pipe_env && stage_ok && nq >= 2 * kChunk;
     cudaEventRecord(h->ev[0], s);
