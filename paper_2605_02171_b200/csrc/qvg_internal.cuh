@@ -118,7 +118,7 @@ struct SearchLaunch {
     const float* qraw;      // non-null: fused encode prologue (raw queries nq x dim);
     float* qn_out;          //   writes normalised queries here, status to out_status
     uint32_t variant;       // A/B switches (QVG_VARIANT env): bit0 no rerank L2 prefetch,
-                            // bit1 paired-half distance pass
+                            // bit1 unused (was: paired-half distance pass)
     uint32_t* exact_bits;   // nullable: per-warp-slot visited bitmaps
     uint64_t exact_words;   // words per slot
     uint32_t depth;         // rerank depth (>= k): the `depth` best scored keys are

@@ -191,7 +191,11 @@ template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = fals
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
-                  const int use_tmap, const uint32_t SL_in) {
+                  const int use_tmap_in, const uint32_t SL_in) {
+    // GEO launches always have the code-row and cold-row tensor maps and never
+    // the exact-visited bitmaps (the host dispatches them only then), so the
+    // fallbacks compile out of the headline kernel
+    const int use_tmap = GEO ? 1 : use_tmap_in;
     const uint32_t SR = GEO ? 32u : SR_in;
     const uint32_t SL = (GEO && SL_in) ? 48u : SL_in;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     uint64_t* pa = pk + ef;  // A
 
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
-    uint32_t* xbits = a.exact_bits ? a.exact_bits + gwarp * a.exact_words : nullptr;
+    uint32_t* xbits = (!GEO && a.exact_bits) ? a.exact_bits + gwarp * a.exact_words : nullptr;
     const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
     // lanes per scored row: the largest power of two with LPR * SR <= 32
     uint32_t lpr_log = 0;
@@ -602,56 +606,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                     ma += __popc(ba);
                 }
             };
-            // paired pass (wait for both halves, then score 2 rows per lane) is
-            // opt-in: measured slower than overlapping half-0 scoring with the
-            // arrival of half 1 (tools/tune_search.py, cfg2: 3.95 vs 3.03 ms)
-            const bool paired = SR <= 32 && (a.variant & 2u);
-            if (paired) {
-                // both halves in flight at once; each lane scores row j of each
-                // half in one pass over the chunks (shared query loads, 2x ILP).
-                // Chunks are visited from a per-lane rotation (bank spreading) as
-                // two straight ranges [rot, W) and [0, rot).
-                for (uint32_t k = 0; k < nsub; k += 2) {
-                    mbar_wait(&bars[0], phs & 1u);
-                    phs ^= 1u;
-                    const bool two = k + 1 < nsub;
-                    if (two) {
-                        mbar_wait(&bars[1], (phs >> 1) & 1u);
-                        phs ^= 2u;
-                    }
-                    const uint32_t cnt0 = min(n - k * SR, SR);
-                    const uint32_t cnt1 = two ? min(n - (k + 1) * SR, SR) : 0u;
-                    const bool v0 = lane < cnt0, v1 = lane < cnt1;
-                    const uint32_t roff = ((lane >> 2) * gstride + (lane & 3u) * rowb) / 16u;
-                    const uint4* r0p = reinterpret_cast<const uint4*>(stage0) + roff;
-                    const uint4* r1p = reinterpret_cast<const uint4*>(stage0 + stage_delta) + roff;
-                    uint32_t d0 = 0, d1 = 0;
-                    if (v0 && v1) {
-#pragma unroll 4
-                        for (uint32_t p = rot; p < W; ++p) {
-                            const uint4 qv = qc[p];
-                            d0 += sm2_chunk(qv, r0p[p]);
-                            d1 += sm2_chunk(qv, r1p[p]);
-                        }
-#pragma unroll 4
-                        for (uint32_t p = 0; p < rot; ++p) {
-                            const uint4 qv = qc[p];
-                            d0 += sm2_chunk(qv, r0p[p]);
-                            d1 += sm2_chunk(qv, r1p[p]);
-                        }
-                    } else if (v0) {
-#pragma unroll 4
-                        for (uint32_t p = rot; p < W; ++p) d0 += sm2_chunk(qc[p], r0p[p]);
-#pragma unroll 4
-                        for (uint32_t p = 0; p < rot; ++p) d0 += sm2_chunk(qc[p], r0p[p]);
-                    }
-                    emit(v0, d0, v0 ? cid[k * SR + lane] : kSentinel);
-                    if (two) emit(v1, d1, v1 ? cid[(k + 1) * SR + lane] : kSentinel);
-                    if (k + 2 < nsub) issue((k + 2) * SR, min(n - (k + 2) * SR, SR), 0);
-                    if (k + 3 < nsub) issue((k + 3) * SR, min(n - (k + 3) * SR, SR), 1);
-                }
-            }
-            for (uint32_t k = 0; !paired && k < nsub; ++k) {
+            // (a paired pass — wait for both halves, then score 2 rows per lane —
+            // measured slower than overlapping half-0 scoring with the arrival of
+            // half 1: cfg2 3.95 vs 3.03 ms; removed)
+            for (uint32_t k = 0; k < nsub; ++k) {
                 const uint32_t h = k & 1u;
                 QVG_PH(long long tw0 = clock64();)
                 mbar_wait(&bars[h], (phs >> h) & 1u);
@@ -1052,7 +1010,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             // rerank: one lane per pool entry, 4 sequential double chains
             const float* qv = a.qn + q * ix.Dp;
             __syncwarp();
-            if (SL) {
+            if (GEO || SL) {
                 // TMA column slices: round t stages slice (t % nsl) of the 32 pool
                 // rows of group (t / nsl) — 4 rows x SL floats per gather4 —
                 // into a stage half; lane r owns row 32g + r and advances its 4
@@ -1201,6 +1159,9 @@ __global__ void pair_distance_kernel(const DevIndex ix, const uint4* __restrict_
     out[t] = d;
 }
 
+// the GEO instantiation compiles out the exact-visited and LDG-rerank paths
+bool geo_allowed(const SearchLaunch& a) { return !a.exact_bits && !(a.variant & 8u); }
+
 uint32_t pow2ceil(uint32_t x) {
     uint32_t p = 1;
     while (p < x) p <<= 1;
@@ -1260,14 +1221,14 @@ uint32_t relaxed_rw(uint32_t R, uint32_t relax) {
 namespace {
 
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap,
-               uint32_t xa, uint32_t relax = 0) {
+               uint32_t xa, uint32_t relax = 0, bool geo_ok = true) {
     Plan p;
     p.rw = relax ? relaxed_rw(ix.R, relax) : pow2ceil((ix.R + 31) / 32);
     p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
-    else if (p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
+    else if (geo_ok && p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
              stage_half_bytes() == 6144)
         p.fn = (void*)search_kernel<2, false, false, 0, 12, true>;
     else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
@@ -1376,7 +1337,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         set_error("search: visited_slots must be >= ef + extra rerank depth (rounded to 32)");
         return QVG_INVALID_ARGUMENT;
     }
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa, a.relax);
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa, a.relax, geo_allowed(a));
     if (p.block_bytes > max_dyn_smem(device)) {
         set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
         return QVG_INVALID_ARGUMENT;
@@ -1408,7 +1369,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
 
 qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_t grid,
                          cudaStream_t s) {
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth), a.relax);
+    const Plan p0 = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth), a.relax, false);
     alignas(64) CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
     const CUtensorMap* m = tmap ? tmap : &dummy;
@@ -1417,13 +1378,16 @@ qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_
     alignas(64) CUtensorMap cmap;
     uint32_t SL = 0;
     if (a.do_rerank && !(a.variant & 8u)) {
-        const uint32_t half = (p.SR / 4u) * group_stride(a.ix.W);
+        const uint32_t half = (p0.SR / 4u) * group_stride(a.ix.W);
         SL = rerank_slice(half);
         if (SL && !encode_rows_map(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.ix.cold, a.ix.Dp,
                                    a.ix.n, SL))
             SL = 0;
     }
     if (!SL) memset(&cmap, 0, sizeof(cmap));
+    // the headline-geometry kernel assumes both tensor maps
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth), a.relax,
+                             geo_allowed(a) && use_tmap && (!a.do_rerank || SL != 0));
     void* args[] = {(void*)m,     (void*)&cmap,     (void*)&a, (void*)&p.warp_bytes,
                     (void*)&p.SR, (void*)&use_tmap, (void*)&SL};
     cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kWarpsPerBlock * 32),

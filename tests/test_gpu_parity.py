@@ -142,14 +142,14 @@ print("OK")
 
 @pytest.mark.parametrize("env", [{"QVG_FUSED": "1"}, {"QVG_ENCODE": "1"}, {"QVG_ENCODE": "2"},
                                  {"QVG_ENCODE": "3"},
-                                 {"QVG_VARIANT": "2"}, {"QVG_VARIANT": "8"},
+                                 {"QVG_VARIANT": "8"},
                                  {"QVG_VARIANT": "13"}, {"QVG_STAGE_HALF_BYTES": "512"},
                                  {"QVG_SPLIT_MAX_ROWS": "32"},
                                  {"QVG_SPLIT_MAX_ROWS": "32", "QVG_STAGE_HALF_BYTES": "512"},
                                  {"QVG_SPLIT_MAX_ROWS": "0"}, {"QVG_COOP_MAX_NQ": "1000000"}])
 def test_opt_in_variants_match_golden(env):
     """The opt-in kernel variants (env switches read once per process): fused
-    encode prologue, tiled / block encoders, paired distance pass, LDG rerank
+    encode prologue, tiled / block encoders, LDG rerank
     fallback (+ no-allocate loads, no L2 prefetch), tiny stage, forced row
     splitting, and the one-CTA-per-query latency kernel.  All bit-exact."""
     import subprocess
