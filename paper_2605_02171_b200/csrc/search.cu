@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         }
 
         // ---- per-query init --------------------------------------------------
-        const long long t_start = clock64();  // phase timers (variant bit 4: debug)
+        // per-query cycle timers (QVG_VARIANT bit 16, debug; not in the GEO kernel)
+        constexpr bool kTimers = !GEO;
+        const long long t_start = kTimers ? clock64() : 0;
 #ifdef QVG_TAIL  // occupancy-over-time build (tools/tail_profile.py): wall-clock span per query
         unsigned long long tg0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
@@ -969,7 +971,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         }
 
         // ---- outputs ------------------------------------------------------------
-        const long long t_search = clock64();
+        const long long t_search = kTimers ? clock64() : 0;
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
         if (a.pool_ids) {
             for (uint32_t i = lane; i < ef; i += 32) {
@@ -1101,8 +1103,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 }
             }
             __syncwarp();
-            const long long t_dots = clock64();
-            if ((a.variant & 16u) && lane == 0 && a.qctr) {
+            const long long t_dots = kTimers ? clock64() : 0;
+            if (kTimers && (a.variant & 16u) && lane == 0 && a.qctr) {
                 a.qctr[q * 8 + 0] = (uint32_t)((t_search - t_start) >> 4);
                 a.qctr[q * 8 + 1] = (uint32_t)((t_dots - t_search) >> 4);
             }
@@ -1127,7 +1129,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             }
             if (lane == 0 && a.out_count) a.out_count[q] = NR < a.k ? NR : a.k;
 #ifndef QVG_PHASES  // slot 2 carries the TMA-issue time in the phases build
-            if ((a.variant & 16u) && lane == 0 && a.qctr)
+            if (kTimers && (a.variant & 16u) && lane == 0 && a.qctr)
                 a.qctr[q * 8 + 2] = (uint32_t)((clock64() - t_dots) >> 4);
 #endif
         }
