@@ -187,7 +187,9 @@ struct MinBlocks {
 // unrolled distance loop).
 // GEO: also the default stage geometry as constants (32 rows per stage half,
 // 48-float rerank slices), dispatched when the launch uses exactly those.
-template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false>
+// PRO: the fused-K1 prologue is compiled in (host queries, pipelined upload);
+// the GEO instantiation for device-resident queries leaves it out.
+template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false, bool PRO = true>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         }
 
         int32_t qst = 0;
-        if (a.qraw) {
+        if (PRO && a.qraw) {
             // fused K1 (encode.cu semantics, bit-exact): the stage is idle
             // between queries and holds the raw row; lane 0 runs the two
             // index-ordered double reductions (vec_math.hpp:28-44,
@@ -1223,7 +1225,7 @@ uint32_t relaxed_rw(uint32_t R, uint32_t relax) {
 namespace {
 
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap,
-               uint32_t xa, uint32_t relax = 0, bool geo_ok = true) {
+               uint32_t xa, uint32_t relax = 0, bool geo_ok = true, bool fused = true) {
     Plan p;
     p.rw = relax ? relaxed_rw(ix.R, relax) : pow2ceil((ix.R + 31) / 32);
     p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
@@ -1232,7 +1234,8 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
     else if (geo_ok && p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
              stage_half_bytes() == 6144)
-        p.fn = (void*)search_kernel<2, false, false, 0, 12, true>;
+        p.fn = fused ? (void*)search_kernel<2, false, false, 0, 12, true, true>
+                     : (void*)search_kernel<2, false, false, 0, 12, true, false>;
     else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
 #ifndef QVG_NO_WC_EXTRA
     else if (p.rw == 1 && !xa && !split && ix.W == 6) p.fn = (void*)search_kernel<1, false, false, 0, 6>;
@@ -1339,7 +1342,8 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         set_error("search: visited_slots must be >= ef + extra rerank depth (rounded to 32)");
         return QVG_INVALID_ARGUMENT;
     }
-    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa, a.relax, geo_allowed(a));
+    const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, xa, a.relax, geo_allowed(a),
+                             a.qraw != nullptr);
     if (p.block_bytes > max_dyn_smem(device)) {
         set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
         return QVG_INVALID_ARGUMENT;
@@ -1389,7 +1393,8 @@ qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_
     if (!SL) memset(&cmap, 0, sizeof(cmap));
     // the headline-geometry kernel assumes both tensor maps
     const Plan p = make_plan(a.ix, a.ef, a.vis_log2, a.tie_cap, extra_depth(a.ef, a.depth), a.relax,
-                             geo_allowed(a) && use_tmap && (!a.do_rerank || SL != 0));
+                             geo_allowed(a) && use_tmap && (!a.do_rerank || SL != 0),
+                             a.qraw != nullptr);
     void* args[] = {(void*)m,     (void*)&cmap,     (void*)&a, (void*)&p.warp_bytes,
                     (void*)&p.SR, (void*)&use_tmap, (void*)&SL};
     cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kWarpsPerBlock * 32),

@@ -457,7 +457,9 @@ def test_relaxed_variant_recall_within_half_point():
     geometry, clustered generator, reference-built graph)."""
     from paper_2605_02171_b200.datasets import mixture
     base, q = mixture(30_000, 384, 300, 0.35, seed=11, nq=1000, sigma_mode="norm")
-    ref = O.RefIndex.build(base, m=16, ef_c=64, alpha=1.2, threads=os.cpu_count())
+    # one build thread: the reference's multi-threaded insertion order is not
+    # deterministic, and the recall comparison must not depend on the graph draw
+    ref = O.RefIndex.build(base, m=16, ef_c=64, alpha=1.2, threads=1)
     ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
     qn, _, _ = Q.encode_queries(q)
     gt = Q.brute_force_topk(ref.cold(), qn, 10)
