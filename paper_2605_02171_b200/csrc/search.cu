@@ -189,15 +189,18 @@ struct MinBlocks {
 // 48-float rerank slices), dispatched when the launch uses exactly those.
 // PRO: the fused-K1 prologue is compiled in (host queries, pipelined upload);
 // the GEO instantiation for device-resident queries leaves it out.
-template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false, bool PRO = true>
+// LEAN: the launch has both tensor maps and no exact-visited bitmaps, so the
+// fallbacks and debug timers compile out (GEO implies it).
+template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false, bool PRO = true,
+          bool LEAN = GEO>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
                   const int use_tmap_in, const uint32_t SL_in) {
-    // GEO launches always have the code-row and cold-row tensor maps and never
+    // LEAN launches always have the code-row and cold-row tensor maps and never
     // the exact-visited bitmaps (the host dispatches them only then), so the
-    // fallbacks compile out of the headline kernel
-    const int use_tmap = GEO ? 1 : use_tmap_in;
+    // fallbacks compile out
+    const int use_tmap = LEAN ? 1 : use_tmap_in;
     const uint32_t SR = GEO ? 32u : SR_in;
     const uint32_t SL = (GEO && SL_in) ? 48u : SL_in;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     uint64_t* pa = pk + ef;  // A
 
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
-    uint32_t* xbits = (!GEO && a.exact_bits) ? a.exact_bits + gwarp * a.exact_words : nullptr;
+    uint32_t* xbits = (!LEAN && a.exact_bits) ? a.exact_bits + gwarp * a.exact_words : nullptr;
     const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
     // lanes per scored row: the largest power of two with LPR * SR <= 32
     uint32_t lpr_log = 0;
@@ -406,8 +409,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
         }
 
         // ---- per-query init --------------------------------------------------
-        // per-query cycle timers (QVG_VARIANT bit 16, debug; not in the GEO kernel)
-        constexpr bool kTimers = !GEO;
+        // per-query cycle timers (QVG_VARIANT bit 16, debug; not in LEAN kernels)
+        constexpr bool kTimers = !LEAN;
         const long long t_start = kTimers ? clock64() : 0;
 #ifdef QVG_TAIL  // occupancy-over-time build (tools/tail_profile.py): wall-clock span per query
         unsigned long long tg0;
@@ -1014,7 +1017,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
             // rerank: one lane per pool entry, 4 sequential double chains
             const float* qv = a.qn + q * ix.Dp;
             __syncwarp();
-            if (GEO || SL) {
+            if (LEAN || SL) {
                 // TMA column slices: round t stages slice (t % nsl) of the 32 pool
                 // rows of group (t / nsl) — 4 rows x SL floats per gather4 —
                 // into a stage half; lane r owns row 32g + r and advances its 4
@@ -1163,8 +1166,15 @@ __global__ void pair_distance_kernel(const DevIndex ix, const uint4* __restrict_
     out[t] = d;
 }
 
-// the GEO instantiation compiles out the exact-visited and LDG-rerank paths
-bool geo_allowed(const SearchLaunch& a) { return !a.exact_bits && !(a.variant & 8u); }
+// LEAN instantiations compile out the exact-visited and LDG-rerank paths
+// (QVG_LEAN=0: never, for A/B)
+bool geo_allowed(const SearchLaunch& a) {
+    static const bool env_ok = [] {
+        const char* e = getenv("QVG_LEAN");
+        return !(e && e[0] == '0');
+    }();
+    return env_ok && !a.exact_bits && !(a.variant & 8u);
+}
 
 uint32_t pow2ceil(uint32_t x) {
     uint32_t p = 1;
@@ -1231,17 +1241,22 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     p.SR = stage_rows_for(ix.W, p.rw * 32, stage_half_bytes());
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
-    else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
     else if (geo_ok && p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
              stage_half_bytes() == 6144)
         p.fn = fused ? (void*)search_kernel<2, false, false, 0, 12, true, true>
                      : (void*)search_kernel<2, false, false, 0, 12, true, false>;
-    else if (p.rw == 2 && !xa && !split && ix.W == 12) p.fn = (void*)search_kernel<2, false, false, 0, 12>;
-#ifndef QVG_NO_WC_EXTRA
-    else if (p.rw == 1 && !xa && !split && ix.W == 6) p.fn = (void*)search_kernel<1, false, false, 0, 6>;
+    else if (p.rw == 2 && !xa && !split && ix.W == 12)
+        p.fn = !geo_ok ? (void*)search_kernel<2, false, false, 0, 12>
+             : fused   ? (void*)search_kernel<2, false, false, 0, 12, false, true, true>
+                       : (void*)search_kernel<2, false, false, 0, 12, false, false, true>;
+    else if (p.rw == 1 && !xa && !split && ix.W == 6)
+        p.fn = !geo_ok ? (void*)search_kernel<1, false, false, 0, 6>
+             : fused   ? (void*)search_kernel<1, false, false, 0, 6, false, true, true>
+                       : (void*)search_kernel<1, false, false, 0, 6, false, false, true>;
+    // (wide-row LEAN instantiations measured 3.6 % slower at W = 48: not used)
     else if (p.rw == 2 && !xa && split && ix.W == 24) p.fn = (void*)search_kernel<2, false, true, 0, 24>;
     else if (p.rw == 2 && !xa && split && ix.W == 48) p.fn = (void*)search_kernel<2, false, true, 0, 48>;
-#endif
+    else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
