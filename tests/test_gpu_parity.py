@@ -483,15 +483,22 @@ def test_headline_code_width_parity_vs_reference(dim, m):
     run_query_batch on a reference-built graph: bit-identical ids and scores,
     identical pools vs the dual-heap oracle."""
     from paper_2605_02171_b200.datasets import mixture
-    base, q = mixture(8_000, dim, 100, 0.3, seed=5, nq=400, sigma_mode="norm")
+    import torch
+    base, q = mixture(8_000, dim, 100, 0.3, seed=5, nq=2_500, sigma_mode="norm")
     ref = O.RefIndex.build(base, m=m, ef_c=64, alpha=1.2, threads=os.cpu_count())
     ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
     orc = O.OracleIndex.from_ref(ref)
+    qd = torch.from_numpy(q).cuda()
     for ef in (16, 64, 128):
         ids, sc, cnt = ref.run_query_batch(q, ef, 10, threads=os.cpu_count())
+        # host queries (>= 2 chunks: pipelined upload + fused encode prologue)
         r = ix.search_ex(q, k=10, ef=ef)
         assert np.array_equal(r["ids"], ids), ef
         assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32)), ef
-        o = orc.query_batch(q, ef, 10, mode=0, pools=True)
-        assert np.array_equal(r["pool_ids"], o["pool_ids"]), ef
-        assert np.array_equal(r["pool_dists"], o["pool_dists"]), ef
+        o = orc.query_batch(q[:400], ef, 10, mode=0, pools=True)
+        assert np.array_equal(r["pool_ids"][:400], o["pool_ids"]), ef
+        assert np.array_equal(r["pool_dists"][:400], o["pool_dists"]), ef
+        # device-resident queries, timing-style launch (no counters, no pools)
+        d_ids, d_sc, _ = ix.search(qd, k=10, ef=ef)
+        assert np.array_equal(d_ids, ids), ef
+        assert np.array_equal(d_sc.view(np.uint32), sc.view(np.uint32)), ef
