@@ -511,11 +511,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
                 guess_idx = kSentinel;
                 for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
                     const uint32_t idx = b0 + lane;
-                    const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
+                    const uint64_t pv = idx < np ? pk[idx] : kExp;
+                    const bool un = idx >= hint && !(pv & kExp);
                     const unsigned bal = __ballot_sync(kFull, un);
                     if (bal) {
-                        guess_idx = b0 + __ffs(bal) - 1;
-                        spec_key = ordk(pk[guess_idx]);
+                        const uint32_t src = __ffs(bal) - 1;
+                        guess_idx = b0 + src;
+                        spec_key = __shfl_sync(kFull, pv, src);  // (exp bit clear)
                         guess = (uint32_t)spec_key;
                         break;
                     }
