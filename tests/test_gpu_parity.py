@@ -502,3 +502,33 @@ def test_headline_code_width_parity_vs_reference(dim, m):
         d_ids, d_sc, _ = ix.search(qd, k=10, ef=ef)
         assert np.array_equal(d_ids, ids), ef
         assert np.array_equal(d_sc.view(np.uint32), sc.view(np.uint32)), ef
+
+
+@pytest.mark.gpu
+@ref_only
+def test_headline_kernel_small_index_and_bad_rows():
+    """The headline-geometry kernels (D = 768, R = 64) on a 300-node index:
+    ef up to N (exhaustive pools equal the dual-heap oracle's), host batches
+    large enough for the pipelined upload with invalid rows (status codes as
+    the reference's exceptions, valid rows unaffected), and the device path."""
+    import torch
+    from paper_2605_02171_b200.datasets import mixture
+    base, q = mixture(300, 768, 10, 0.3, seed=9, nq=2_100, sigma_mode="norm")
+    ref = O.RefIndex.build(base, m=32, ef_c=64, alpha=1.2, threads=1)
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    orc = O.OracleIndex.from_ref(ref)
+    bad = q.copy()
+    bad[7] = 0.0
+    bad[2049, 100] = np.inf
+    ok = np.ones(len(q), bool)
+    ok[[7, 2049]] = False
+    for ef in (10, 100, 300):
+        o = orc.query_batch(q, ef, 10, mode=0, pools=True)
+        r = ix.search_ex(bad, k=10, ef=ef, check=False)  # host, >= 2 chunks: pipelined
+        assert r["rc"] == Q.N.QVG_INVALID_ARGUMENT
+        assert r["status"][7] == 2 and r["status"][2049] == 1
+        assert np.array_equal(r["ids"][ok], o["ids"][ok]), ef
+        assert np.array_equal(r["scores"][ok].view(np.uint32), o["scores"][ok].view(np.uint32)), ef
+        assert np.array_equal(r["pool_ids"][ok], o["pool_ids"][ok]), ef
+        d_ids, d_sc, _ = ix.search(torch.from_numpy(q).cuda(), k=10, ef=ef)
+        assert np.array_equal(d_ids, o["ids"]) and np.array_equal(d_sc.view(np.uint32), o["scores"].view(np.uint32))
