@@ -112,7 +112,8 @@ struct SmemLayout {
 // candidate buffers.
 __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uint32_t W,
                                                   uint32_t tie_cap, uint32_t vis_slots,
-                                                  uint32_t stage_rows, uint32_t xa = 0) {
+                                                  uint32_t stage_rows, uint32_t xa = 0,
+                                                  bool lean_ranks = false) {
     SmemLayout L;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -128,8 +129,11 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.ctd = take(8 * RM, 16);    // contenders, row order
     L.evk = L.ctd;               // keys evicted this step (ctd is dead by then)
     L.crp = take(4 * RM, 16);    // contender rank in P, row order
-    L.csrp = take(4 * RM, 16);   // contender rank in P, key order
+    // contender rank in P, key order (lean_ranks: in the compacted-id buffer,
+    // which is dead between the last distance pass and the next compaction)
+    L.csrp = lean_ranks ? 0 : take(4 * RM, 16);
     L.cid = take(4 * RM, 16);    // compacted row ids to score
+    if (lean_ranks) L.csrp = L.cid;
     L.stg = L.crp;               // tie-stack additions (crp is dead by then)
     L.qc = take(16 * W, 16);     // query code chunks
     L.tie = take(4 * tie_cap, 16);
@@ -164,7 +168,7 @@ template <int RW, int RELP = 0>
 #endif
 struct MinBlocks {
     static constexpr int value =
-        RELP ? (RW <= 2 ? 8 : 6) : (RW == 1 ? 9 : (RW == 2 ? QVG_MINBLOCKS_RW2 : 5));
+        RELP ? (RW <= 2 ? 8 : 7) : (RW == 1 ? 9 : (RW == 2 ? QVG_MINBLOCKS_RW2 : 5));
 };
 
 // XA: rerank deeper than ef.  A = the best `xa` scored keys outside P, kept
@@ -219,7 +223,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     const uint32_t ef = a.ef;  // (a compile-time ef = 64 instantiation measured +0.3 %)
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa);
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, REL);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -1262,7 +1266,7 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
-                                     1u << vis_log2, p.SR, xa);
+                                     1u << vis_log2, p.SR, xa, relax != 0);
     p.warp_bytes = L.total;
     p.block_bytes = p.warp_bytes * kWarpsPerBlock;
     return p;
@@ -1329,7 +1333,7 @@ uint32_t search_stage_bytes(const DevIndex& ix) {
 
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
                            uint32_t xa, uint32_t relax) {
-    uint32_t min_log = 8;  // 256 slots
+    uint32_t min_log = relax ? 7 : 8;  // 256 slots (relaxed: 128, for its wider contender buffers)
     while ((1u << min_log) < ((ef + xa + 31u) & ~31u)) ++min_log;  // rerank scores alias it
     uint32_t best_log = min_log;
     int best_blocks = -1;
