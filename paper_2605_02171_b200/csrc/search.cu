@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     const uint32_t ef = a.ef;  // (a compile-time ef = 64 instantiation measured +0.3 %)
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, REL);
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, true);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -1266,7 +1266,7 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
-                                     1u << vis_log2, p.SR, xa, relax != 0);
+                                     1u << vis_log2, p.SR, xa, true);
     p.warp_bytes = L.total;
     p.block_bytes = p.warp_bytes * kWarpsPerBlock;
     return p;
@@ -1333,7 +1333,7 @@ uint32_t search_stage_bytes(const DevIndex& ix) {
 
 uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, int device,
                            uint32_t xa, uint32_t relax) {
-    uint32_t min_log = relax ? 7 : 8;  // 256 slots (relaxed: 128, for its wider contender buffers)
+    uint32_t min_log = 7;  // 128 slots
     while ((1u << min_log) < ((ef + xa + 31u) & ~31u)) ++min_log;  // rerank scores alias it
     uint32_t best_log = min_log;
     int best_blocks = -1;
