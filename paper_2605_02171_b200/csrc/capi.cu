@@ -40,6 +40,17 @@ qvg_status grow(Buffer& b, size_t bytes) {
     return QVG_OK;
 }
 
+// page-locked host memory (cudaHostAlloc / cudaHostRegister)
+bool is_pinned_host_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes at;
@@ -351,12 +362,16 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     bool coop = coop_env != 0 && pinfo.coop_cap > 0 && !a.exact_bits && !a.qraw && !a.ready &&
                 !(a.do_rerank && a.depth != a.ef) && !a.relax;
     if (coop) coop = coop_env > 0 ? nq <= (uint64_t)coop_env : nq <= pinfo.coop_cap;
-    if (pipelined) {
-        // The chunk copies are submitted BEFORE the search launch: in normal
-        // operation the copy engine still overlaps them with the running
-        // kernel (each warp waits only for its own query's chunk), and a tool
-        // that serialises launches (ncu kernel replay, compute-sanitizer)
-        // drains them before the kernel starts instead of deadlocking it.
+    // Chunk copies of a PINNED buffer are submitted BEFORE the search launch
+    // (pure DMA, submission is cheap): the copy engine still overlaps them with
+    // the running kernel, and a tool that serialises launches (ncu kernel
+    // replay, compute-sanitizer) drains them before the kernel starts instead
+    // of deadlocking it.  A PAGEABLE buffer is staged by the host thread inside
+    // each cudaMemcpyAsync, so its chunks are submitted after the launch (the
+    // kernel runs while the driver stages them); under such tools use
+    // QVG_PIPELINE=0 for pageable host queries.
+    const bool copies_first = pipelined && is_pinned_host_ptr(user_in);
+    auto submit_chunks = [&]() -> qvg_status {
         // Each chunk's ready count is a 4-byte copy ordered after its rows on
         // the copy stream; the chunks start after the counter reset (ev[1]).
         cudaStream_t cs = h->copy_stream;
@@ -372,17 +387,28 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
                 e = cudaMemcpyAsync(d_ready, &h->ready_host[c], 4, cudaMemcpyHostToDevice, cs);
             }
             if (e != cudaSuccess) {
-                cudaStreamSynchronize(cs);  // no kernel was launched yet: nothing waits
+                // never leave a running kernel waiting: release every query
+                // (a copy-engine write; no SM is free while the search runs)
+                if (!copies_first) {
+                    const uint64_t last = (nq + kChunk - 1) / kChunk - 1;
+                    h->ready_host[last] = (uint32_t)nq;
+                    cudaMemcpyAsync(d_ready, &h->ready_host[last], 4, cudaMemcpyHostToDevice, cs);
+                }
+                cudaStreamSynchronize(cs);
+                if (!copies_first) cudaStreamSynchronize(s);
                 return cuda_status(e, "H2D(queries, pipelined)");
             }
         }
         cudaEventRecord(h->ev_copy, cs);
-    }
+        return QVG_OK;
+    };
+    if (copies_first && (st = submit_chunks()) != QVG_OK) return st;
     if (coop) {
         if ((st = launch_coop(a, &h->tmap, s, h->device)) != QVG_OK) return st;
     } else if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) {
         return st;
     }
+    if (pipelined && !copies_first && (st = submit_chunks()) != QVG_OK) return st;
     if (pipelined) cudaStreamWaitEvent(s, h->ev_copy, 0);  // results after every chunk
     cudaEventRecord(h->ev[3], s);
     Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
