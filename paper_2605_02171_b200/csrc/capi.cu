@@ -404,8 +404,12 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     };
     if (copies_first && (st = submit_chunks()) != QVG_OK) return st;
     if (coop) {
-        if ((st = launch_coop(a, &h->tmap, s, h->device)) != QVG_OK) return st;
-    } else if ((st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s)) != QVG_OK) {
+        st = launch_coop(a, &h->tmap, s, h->device);
+    } else {
+        st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s);
+    }
+    if (st != QVG_OK) {
+        if (copies_first) cudaStreamSynchronize(h->copy_stream);  // no copy outlives the call
         return st;
     }
     if (pipelined && !copies_first && (st = submit_chunks()) != QVG_OK) return st;
