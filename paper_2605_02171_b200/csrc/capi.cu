@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <unistd.h>  // environ
 #include <string>
 #include <vector>
 
@@ -38,6 +39,22 @@ qvg_status grow(Buffer& b, size_t bytes) {
     if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(scratch)");
     b.bytes = want;
     return QVG_OK;
+}
+
+// a tool that serialises kernel launches is injected (Nsight Compute sets
+// NV_NSIGHT_INJECTION_* / NV_TPS_LAUNCH_TOKEN; CUDA_INJECTION64_PATH is the
+// generic injection hook; sanitizer variables): the pipelined upload must then
+// submit its copies before the launch whatever the buffer type
+bool under_tool() {
+    static const bool v = [] {
+        if (getenv("CUDA_INJECTION64_PATH") || getenv("NV_TPS_LAUNCH_TOKEN") ||
+            getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+            return true;
+        for (char** e = ::environ; e && *e; ++e)
+            if (strstr(*e, "SANITIZER") || strstr(*e, "NSIGHT_INJECTION")) return true;
+        return false;
+    }();
+    return v;
 }
 
 // page-locked host memory (cudaHostAlloc / cudaHostRegister)
@@ -370,7 +387,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     // each cudaMemcpyAsync, so its chunks are submitted after the launch (the
     // kernel runs while the driver stages them); under such tools use
     // QVG_PIPELINE=0 for pageable host queries.
-    const bool copies_first = pipelined && is_pinned_host_ptr(user_in);
+    const bool copies_first = pipelined && (is_pinned_host_ptr(user_in) || under_tool());
     auto submit_chunks = [&]() -> qvg_status {
         // Each chunk's ready count is a 4-byte copy ordered after its rows on
         // the copy stream; the chunks start after the counter reset (ev[1]).
