@@ -22,7 +22,7 @@ MARKERS = [  # (substring of the first line of a region, region name), in file o
     ("// (a) TMA-gather", "tma issue call"),
     ("// speculative prefetch", "spec adjacency"),
     ("// (b) SM2 distances", "emit"),
-    ("// paired pass", "distance loop"),
+    ("// (a paired pass", "distance loop"),
     ("// (c) contender ranks", "ranks"),
     ("// (d) in-place merge", "merge"),
     ("// (e) tie stack", "tie"),
