@@ -570,7 +570,8 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
             cudaMemsetAsync(d_ctr, 0, 8, s);
             sa.nq = nb;
             sa.ix = ix;
-            uint64_t g = (nb + kWarpsPerBlock - 1) / kWarpsPerBlock;
+            const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
+            uint64_t g = (nb + wpb - 1) / wpb;
             if (g > grid_full) g = grid_full;
             if ((st = launch_search(sa, h->has_tmap ? &h->tmap : nullptr, g, s)) != QVG_OK) return fail(st);
             // 2. forward prune over the pool (+ current row on later passes)

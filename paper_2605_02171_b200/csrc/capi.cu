@@ -301,14 +301,16 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
             it = h->plans.emplace(key, std::make_pair(vlog, pinfo)).first;
         }
         pinfo = it->second.second;
-        const uint64_t want = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        const uint64_t full = (uint64_t)pinfo.resident_warps_per_sm / kWarpsPerBlock * pinfo.sms;
+        const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
+        const uint64_t want = (nq + wpb - 1) / wpb;
+        const uint64_t full = (uint64_t)pinfo.resident_warps_per_sm / wpb * pinfo.sms;
         grid = want < full ? want : full;
         if (grid < 1) grid = 1;
     }
     if (exact) {
         const uint64_t words = ((ix.n + 31) / 32 + 3) & ~3ull;
-        if ((st = grow(h->s_exact, grid * kWarpsPerBlock * words * 4)) != QVG_OK) return st;
+        const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
+        if ((st = grow(h->s_exact, grid * wpb * words * 4)) != QVG_OK) return st;
         a.exact_bits = static_cast<uint32_t*>(h->s_exact.p);
         a.exact_words = words;
     }

@@ -17,6 +17,7 @@ constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr uint32_t kMaxEf = 1024;
 constexpr uint32_t kMaxDegree = 128;
 constexpr int kWarpsPerBlock = 2;
+constexpr int kGeoMaxWarps = 16;  // headline-geometry kernel: one block per SM, up to 16 warps
 
 // HBM-resident index.  Layouts:
 //   codes : n x W chunks of 16 B, chunk w = {pos word w, strong word w}

@@ -113,7 +113,7 @@ struct SmemLayout {
 __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uint32_t W,
                                                   uint32_t tie_cap, uint32_t vis_slots,
                                                   uint32_t stage_rows, uint32_t xa = 0,
-                                                  bool lean_ranks = false) {
+                                                  bool lean_ranks = false, bool geo = false) {
     SmemLayout L;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes, uint32_t align) {
@@ -122,9 +122,12 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
         o += bytes;
         return at;
     };
-    L.bars = take(16, 16);
+    // geo: the stage first (no alignment gap) and the rerank query slices in
+    // the contender buffer (dead during the rerank) — 496 B less per warp
+    if (!geo) L.bars = take(16, 16);
     L.stage0 = take((stage_rows / 4) * group_stride(W), 128);
     L.stage1 = take((stage_rows / 4) * group_stride(W), 128);
+    if (geo) L.bars = take(16, 16);
     L.pk = take(8 * EFM, 16);    // pool keys P[0, ef), then extra-depth keys A
     L.ctd = take(8 * RM, 16);    // contenders, row order
     L.evk = L.ctd;               // keys evicted this step (ctd is dead by then)
@@ -138,7 +141,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.qc = take(16 * W, 16);     // query code chunks
     L.tie = take(4 * tie_cap, 16);
     L.vis = take(4 * vis_slots, 16);  // rerank scores alias this region (vis_slots >= EFM)
-    L.qsl = take(2 * 48 * 4, 16);     // rerank query slices (one per stage half)
+    L.qsl = geo && 8 * RM >= 2 * 48 * 4 ? L.ctd : take(2 * 48 * 4, 16);  // rerank query slices
     // extra depth: A candidates of one step (<= RM: each scored key is a P
     // contender or an A candidate, and evictions <= P contenders), sorted copy
     // and their ranks in A
@@ -197,7 +200,8 @@ struct MinBlocks {
 // fallbacks and debug timers compile out (GEO implies it).
 template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false, bool PRO = true,
           bool LEAN = GEO>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::value)
+__global__ void __launch_bounds__(GEO ? kGeoMaxWarps * 32 : kWarpsPerBlock * 32,
+                                  GEO ? 1 : MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
                   const int use_tmap_in, const uint32_t SL_in) {
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     const uint32_t ef = a.ef;  // (a compile-time ef = 64 instantiation measured +0.3 %)
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, true);
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, true, GEO);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MinBlocks<RW, RELP>::valu
     uint32_t* axr = reinterpret_cast<uint32_t*>(base + L.axr);
     uint64_t* pa = pk + ef;  // A
 
-    const uint64_t gwarp = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
     uint32_t* xbits = (!LEAN && a.exact_bits) ? a.exact_bits + gwarp * a.exact_words : nullptr;
     const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
     // lanes per scored row: the largest power of two with LPR * SR <= 32
@@ -1200,6 +1204,8 @@ uint32_t stage_half_bytes() {
 struct Plan {
     void* fn;
     uint32_t rw, SR, warp_bytes, block_bytes;
+    bool geo = false;               // the headline-geometry instantiation (GEO)
+    uint32_t wpb = kWarpsPerBlock;  // warps per block (GEO: one block per SM, as many as fit)
 };
 
 // split rows over lanes when a stage half holds at most this many rows
@@ -1249,8 +1255,11 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (geo_ok && p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
              stage_half_bytes() == 6144)
+    {
         p.fn = fused ? (void*)search_kernel<2, false, false, 0, 12, true, true>
                      : (void*)search_kernel<2, false, false, 0, 12, true, false>;
+        p.geo = true;
+    }
     else if (p.rw == 2 && !xa && !split && ix.W == 12)
         p.fn = !geo_ok ? (void*)search_kernel<2, false, false, 0, 12>
              : fused   ? (void*)search_kernel<2, false, false, 0, 12, false, true, true>
@@ -1266,9 +1275,30 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
-                                     1u << vis_log2, p.SR, xa, true);
+                                     1u << vis_log2, p.SR, xa, true, p.geo);
     p.warp_bytes = L.total;
-    p.block_bytes = p.warp_bytes * kWarpsPerBlock;
+    if (p.geo) {
+        // one block per SM with as many warps as its shared memory holds (the
+        // 1 KB per-block reservation is paid once instead of per 2-warp block)
+        static const uint32_t sm_smem = [] {
+            int d = 0, v = 0, r = 0;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, d);
+            cudaDeviceGetAttribute(&r, cudaDevAttrReservedSharedMemoryPerBlock, d);
+            return (uint32_t)(v > r ? v - r : 0);
+        }();
+        static const uint32_t blk_smem = [] {
+            int d = 0, v = 0;
+            cudaGetDevice(&d);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+            return (uint32_t)v;
+        }();
+        uint32_t w = sm_smem / p.warp_bytes;
+        if (w * p.warp_bytes > blk_smem) w = blk_smem / p.warp_bytes;
+        if (w > (uint32_t)kGeoMaxWarps) w = kGeoMaxWarps;
+        p.wpb = w < 1 ? 1 : w;
+    }
+    p.block_bytes = p.warp_bytes * p.wpb;
     return p;
 }
 
@@ -1343,11 +1373,12 @@ uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, in
             break;
         }
         int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, p.fn, kWarpsPerBlock * 32,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, p.fn, p.wpb * 32,
                                                           p.block_bytes) != cudaSuccess) {
             cudaGetLastError();
             break;
         }
+        blocks *= (int)p.wpb;         // resident warps
         if (blocks >= best_blocks) {  // ties go to the larger table
             best_blocks = blocks;
             best_log = lg;
@@ -1372,7 +1403,7 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
     if (!allow_max_smem(p.fn, device)) return cuda_status(cudaGetLastError(), "cudaFuncSetAttribute");
     cudaError_t e;
     int per_sm = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.fn, kWarpsPerBlock * 32,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.fn, p.wpb * 32,
                                                       p.block_bytes);
     if (e != cudaSuccess) return cuda_status(e, "occupancy(search)");
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1380,15 +1411,15 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         set_error("search: per-warp shared memory too large (reduce visited_slots / tie_capacity)");
         return QVG_INVALID_ARGUMENT;
     }
-    uint64_t want = (a.nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    uint64_t want = (a.nq + p.wpb - 1) / p.wpb;
     uint64_t grid = (uint64_t)per_sm * sms;
     if (want < grid) grid = want;
     if (grid < 1) grid = 1;
     *grid_out = grid;
     if (info) {
-        info->warps_per_block = kWarpsPerBlock;
+        info->warps_per_block = p.wpb;
         info->smem_per_block = p.block_bytes;
-        info->resident_warps_per_sm = (uint32_t)per_sm * kWarpsPerBlock;
+        info->resident_warps_per_sm = (uint32_t)per_sm * p.wpb;
         info->sms = (uint32_t)sms;
     }
     return QVG_OK;
@@ -1418,7 +1449,7 @@ qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_
                              a.qraw != nullptr);
     void* args[] = {(void*)m,     (void*)&cmap,     (void*)&a, (void*)&p.warp_bytes,
                     (void*)&p.SR, (void*)&use_tmap, (void*)&SL};
-    cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kWarpsPerBlock * 32),
+    cudaError_t e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(p.wpb * 32),
                                      args, p.block_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "launch(search)");
     return QVG_OK;
