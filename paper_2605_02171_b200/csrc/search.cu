@@ -198,10 +198,12 @@ struct MinBlocks {
 // the GEO instantiation for device-resident queries leaves it out.
 // LEAN: the launch has both tensor maps and no exact-visited bitmaps, so the
 // fallbacks and debug timers compile out (GEO implies it).
+// ONE: one block per SM with as many warps as fit (GEO implies it), for the
+// wide-row geometries whose per-warp shared memory leaves few warps per SM.
 template <int RW, bool XA, bool SPLIT, int RELP = 0, int WC = 0, bool GEO = false, bool PRO = true,
-          bool LEAN = GEO>
-__global__ void __launch_bounds__(GEO ? kGeoMaxWarps * 32 : kWarpsPerBlock * 32,
-                                  GEO ? 1 : MinBlocks<RW, RELP>::value)
+          bool LEAN = GEO, bool ONE = GEO>
+__global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBlock * 32,
+                                  (GEO || ONE) ? 1 : MinBlocks<RW, RELP>::value)
     search_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap cmap,
                   const SearchLaunch a, const uint32_t warp_bytes, const uint32_t SR_in,
                   const int use_tmap_in, const uint32_t SL_in) {
@@ -1205,6 +1207,7 @@ struct Plan {
     void* fn;
     uint32_t rw, SR, warp_bytes, block_bytes;
     bool geo = false;               // the headline-geometry instantiation (GEO)
+    bool one = false;               // one block per SM (ONE) without the GEO layout
     uint32_t wpb = kWarpsPerBlock;  // warps per block (GEO: one block per SM, as many as fit)
 };
 
@@ -1246,6 +1249,15 @@ uint32_t relaxed_rw(uint32_t R, uint32_t relax) {
 
 namespace {
 
+// QVG_ONEBLK=0: the wide-row kernels keep 2-warp blocks (A/B measurement)
+bool one_block_ok() {
+    static const bool ok = [] {
+        const char* e = getenv("QVG_ONEBLK");
+        return !(e && e[0] == '0');
+    }();
+    return ok;
+}
+
 Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_cap,
                uint32_t xa, uint32_t relax = 0, bool geo_ok = true, bool fused = true) {
     Plan p;
@@ -1269,15 +1281,22 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
              : fused   ? (void*)search_kernel<1, false, false, 0, 6, false, true, true>
                        : (void*)search_kernel<1, false, false, 0, 6, false, false, true>;
     // (wide-row LEAN instantiations measured 3.6 % slower at W = 48: not used)
-    else if (p.rw == 2 && !xa && split && ix.W == 24) p.fn = (void*)search_kernel<2, false, true, 0, 24>;
-    else if (p.rw == 2 && !xa && split && ix.W == 48) p.fn = (void*)search_kernel<2, false, true, 0, 48>;
+    else if (p.rw == 2 && !xa && split && ix.W == 24) {
+        p.one = one_block_ok();
+        p.fn = p.one ? (void*)search_kernel<2, false, true, 0, 24, false, true, false, true>
+                     : (void*)search_kernel<2, false, true, 0, 24>;
+    } else if (p.rw == 2 && !xa && split && ix.W == 48) {
+        p.one = one_block_ok();
+        p.fn = p.one ? (void*)search_kernel<2, false, true, 0, 48, false, true, false, true>
+                     : (void*)search_kernel<2, false, true, 0, 48>;
+    }
     else if (p.rw == 1) p.fn = pick_kernel<1>(xa != 0, split);
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
                                      1u << vis_log2, p.SR, xa, true, p.geo);
     p.warp_bytes = L.total;
-    if (p.geo) {
+    if (p.geo || p.one) {
         // one block per SM with as many warps as its shared memory holds (the
         // 1 KB per-block reservation is paid once instead of per 2-warp block)
         static const uint32_t sm_smem = [] {

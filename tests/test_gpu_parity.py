@@ -532,3 +532,34 @@ def test_headline_kernel_small_index_and_bad_rows():
         assert np.array_equal(r["pool_ids"][ok], o["pool_ids"][ok]), ef
         d_ids, d_sc, _ = ix.search(torch.from_numpy(q).cuda(), k=10, ef=ef)
         assert np.array_equal(d_ids, o["ids"]) and np.array_equal(d_sc.view(np.uint32), o["scores"].view(np.uint32))
+
+
+@pytest.mark.gpu
+@ref_only
+@pytest.mark.parametrize("dim", [1536, 3072])
+def test_wide_row_one_block_kernels_vs_reference(dim):
+    """The wide-row split kernels (W = 24 at D = 1536, W = 48 at D = 3072,
+    R = 64) launched as one block per SM with as many warps as fit (the
+    `ONE` instantiations) against the reference's own run_query_batch on a
+    reference-built graph: identical ids, bit-identical scores, identical
+    pools vs the dual-heap oracle; host and device-resident queries."""
+    from paper_2605_02171_b200.datasets import mixture
+    import torch
+    base, q = mixture(3_000, dim, 60, 0.3, seed=11, nq=1_500, sigma_mode="norm")
+    ref = O.RefIndex.build(base, m=32, ef_c=64, alpha=1.2, threads=os.cpu_count())
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    orc = O.OracleIndex.from_ref(ref)
+    qd = torch.from_numpy(q).cuda()
+    for ef in (16, 64, 200):
+        ids, sc, _ = ref.run_query_batch(q, ef, 10, threads=os.cpu_count())
+        r = ix.search_ex(q, k=10, ef=ef)
+        print(dim, ef, {k_: r["stats"][k_] for k_ in ("warps_per_block", "resident_warps_per_sm")})
+        assert r["stats"]["warps_per_block"] > 2, r["stats"]  # one block per SM
+        assert np.array_equal(r["ids"], ids), ef
+        assert np.array_equal(r["scores"].view(np.uint32), sc.view(np.uint32)), ef
+        o = orc.query_batch(q[:200], ef, 10, mode=0, pools=True)
+        assert np.array_equal(r["pool_ids"][:200], o["pool_ids"]), ef
+        assert np.array_equal(r["pool_dists"][:200], o["pool_dists"]), ef
+        d_ids, d_sc, _ = ix.search(qd, k=10, ef=ef)
+        assert np.array_equal(d_ids, ids), ef
+        assert np.array_equal(d_sc.view(np.uint32), sc.view(np.uint32)), ef
