@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--relaxed", default="2",
                     help="relaxed-variant rows at the headline ef: expansions per step "
                          "list ('2', '2,4', 'none'); reported separately, never parity")
+    ap.add_argument("--depth-parity-queries", type=int, default=500,
+                    help="queries checked against orc_query_depth per rerank-depth row")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
 
@@ -78,8 +80,11 @@ def log(*a):
         print(*a, file=sys.stderr, flush=True)
 
 
-def load_workload(args):
-    from paper_2605_02171_b200 import datasets, graphs
+def load_workload(args, allow_gpu_build=True):
+    """-> (cfg, base, queries, adjacency, entry, provenance).  The reference arm
+    passes allow_gpu_build=False: it never imports the product package, and
+    without a cached graph it builds one with the reference builder."""
+    from workloads import datasets, graphs
     cfg = datasets.CONFIGS[args.config]
     t0 = time.time()
     base, queries = datasets.config_data(cfg, n=args.n, nq=args.nq, sigma_mode=args.sigma_mode)
@@ -89,6 +94,14 @@ def load_workload(args):
     if g is None:
         g = graphs.load_graph(cfg, args.sigma_mode, base.shape[0], base, builder="gpu")
         provenance = "GPU builder qvg_build (cached, data_cache/)"
+    if g is None and not allow_gpu_build:
+        from oracle.oracle import RefIndex
+        log("[bench] no cached graph: building with the reference builder")
+        t0 = time.time()
+        ref = RefIndex.build(base, m=cfg.m, ef_c=cfg.ef_c, alpha=cfg.alpha, seed=42)
+        g = dict(adj=ref.adjacency(), entry=np.uint32(ref.entry))
+        provenance = f"reference qivr::build_index (built in this run, {time.time() - t0:.0f}s)"
+        ref.close()
     if g is None:
         import paper_2605_02171_b200 as Q
         log("[bench] no cached graph: building on the GPU (qvg_build)")
@@ -202,22 +215,97 @@ def recall_at_k(res, gt, k):
 
 
 # ----------------------------------------------------------------------------
-def run_reference_search(args, cfg, base, queries, adj, entry, k, ef, budget_s=60.0,
-                         steps=None, warmup=0):
-    """The reference's CPU path: qivr::run_query_batch on the same graph."""
-    from oracle.oracle import RefIndex
-    threads = os.cpu_count() or 1
-    t0 = time.time()
-    ref = RefIndex.from_graph(base, adj, cfg.m, entry, cfg.alpha, threads=threads)
-    log(f"[bench] reference index (stage0 + cached graph) in {time.time() - t0:.1f}s")
-    # calibrate a bounded per-step sample
-    t0 = time.time()
-    ref.run_query_batch(queries[:256], ef, k, threads=threads)
-    est = 256 / max(time.time() - t0, 1e-6)
-    return ref, threads, est
+L2_NOTE = ("GPU arm: L2 flushed between steps (256 MB write); "
+           "reference arm: CPU, host caches not flushed")
+
+
+def bench_config(args, cfg, n, D, nq, provenance):
+    """The `config` object — byte-identical in both arms (same workload, same graph)."""
+    return {"workload": f"cfg{args.config}: N={n} D={D} R={2 * cfg.m} L={cfg.ef_c} "
+                        f"alpha={cfg.alpha} nq={nq} ef={args.ef} k={args.k} "
+                        f"sigma={cfg.sigma} ({args.sigma_mode})",
+            "graph": provenance, "l2": L2_NOTE}
+
+
+def cpu_info():
+    """Host CPU of the baseline: model, physical cores, logical CPUs, SMT, and the
+    threads this process may run on (the count the baseline uses)."""
+    model, phys, cores, logical = None, None, set(), 0
+    try:
+        for ln in open("/proc/cpuinfo"):
+            key, _, v = ln.partition(":")
+            key, v = key.strip(), v.strip()
+            if key == "processor":
+                logical += 1
+            elif key == "model name" and model is None:
+                model = v
+            elif key == "physical id":
+                phys = v
+            elif key == "core id":
+                cores.add((phys, v))
+    except Exception:
+        pass
+    usable = (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+              else os.cpu_count() or 1)
+    physical = len(cores) or None
+    return {"model": model, "logical_cpus": logical or os.cpu_count(),
+            "physical_cores": physical,
+            "smt": None if physical is None else bool(logical > physical),
+            "threads_used": usable}
+
+
+class RefRunner:
+    """The reference's own CPU path — qivr::run_query_batch from oracle/_ref (the
+    unmodified reference compiled from its sources) — on the same graph and
+    queries.  Results are cached per ef: they are the parity oracle of every
+    timed GPU row."""
+
+    def __init__(self, cfg, base, adj, entry, threads):
+        from oracle.oracle import RefIndex
+        t0 = time.time()
+        self.ref = RefIndex.from_graph(base, adj, cfg.m, entry, cfg.alpha, threads=threads)
+        log(f"[bench] reference index (stage0 + cached graph) in {time.time() - t0:.1f}s")
+        self.threads = threads
+        self.cache = {}
+
+    def results(self, queries, ef, k):
+        if ef not in self.cache:
+            self.cache[ef] = self.ref.run_query_batch(queries, ef, k, threads=self.threads)
+        return self.cache[ef]
+
+    def timed(self, queries, ef, k, threads=None):
+        t0 = time.time()
+        r = self.ref.run_query_batch(queries, ef, k, threads=threads or self.threads)
+        return r, time.time() - t0
+
+    def oracle_view(self):
+        """Plain-C restatement over the reference's own stores (for the GPU-only
+        rerank-depth rows, which have no reference counterpart)."""
+        from oracle.oracle import OracleIndex
+        return OracleIndex.from_ref(self.ref)
+
+
+def parity(got, want, rows=None):
+    """ids / score bit patterns / counts of one timed output vs the reference,
+    compared over each query's first count[i] (= reference count) entries."""
+    ids, sc, cnt = (np.asarray(x) for x in got)
+    rids, rsc, rcnt = want
+    if rows is not None:
+        rids, rsc, rcnt = rids[rows], rsc[rows], rcnt[rows]
+    ids = ids.view(np.uint32).reshape(rids.shape)
+    sc = sc.view(np.uint32).reshape(rsc.shape)
+    cnt = cnt.view(np.uint32).reshape(rcnt.shape)
+    mask = np.arange(rids.shape[1])[None, :] < rcnt[:, None]
+    ok_ids = np.where(mask, ids == rids, True).all(axis=1) & (cnt == rcnt)
+    ok_sc = np.where(mask, sc == rsc.view(np.uint32), True).all(axis=1) & (cnt == rcnt)
+    return {"queries": int(rids.shape[0]), "ids_identical": float(ok_ids.mean()),
+            "scores_bit_identical": float(ok_sc.mean()),
+            "counts_identical": float((cnt == rcnt).mean())}
 
 
 def ours(args):
+    import ctypes as C
+
     import torch
 
     import paper_2605_02171_b200 as Q
@@ -260,18 +348,25 @@ def ours(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     opts = N.qvg_search_opts(visited_slots=args.visited_slots, entry_point=N.SENTINEL,
                              timing_only=1)
-    import ctypes as C
 
-    def step_dev(efv=ef, o=opts):
+    def dev_out():
+        """the last timed device launch's outputs (host copies)"""
+        torch.cuda.synchronize()
+        return (ids_d.cpu().numpy().view(np.uint32).copy(), sc_d.cpu().numpy().copy(),
+                cnt_d.cpu().numpy().view(np.uint32).copy())
+
+    def step_dev(efv=ef, o=opts, q_ptr=None, nqv=None):
         st = N.qvg_stats()
-        rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr(), nq, k, efv, C.byref(o),
-                                   ids_d.data_ptr(), sc_d.data_ptr(), cnt_d.data_ptr(),
-                                   st_d.data_ptr(), None, None, None, None, C.byref(st))
+        rc = N.lib().qvg_search_ex(ix._h, q_ptr or q_dev.data_ptr(), nqv or nq, k, efv,
+                                   C.byref(o), ids_d.data_ptr(), sc_d.data_ptr(),
+                                   cnt_d.data_ptr(), st_d.data_ptr(), None, None, None, None,
+                                   C.byref(st))
         if rc:
             raise RuntimeError(N.last_error())
         return st
 
     def step_e2e():
+        # the public drop-in call (qvg_search = run_query_batch) on pinned host buffers
         rc = N.lib().qvg_search(ix._h, q_host.data_ptr(), nq, k, ef, ids_h.data_ptr(),
                                 sc_h.data_ptr(), cnt_h.data_ptr(), None, None)
         if rc:
@@ -313,9 +408,11 @@ def ours(args):
         step_e2e()
     sampler = ClockSampler(local)
     tot_ms, ms, kern_ms, clocks = timed(step_dev, args.steps, sampler)
+    out_dev = dev_out()
     e2e_ms, _, _, _ = timed(step_e2e, args.steps)
-    ids = ids_d.cpu().numpy().view(np.uint32)
-    assert np.array_equal(ids, ex["ids"]), "timed results differ from the stats pass"
+    out_e2e = (ids_h.numpy().view(np.uint32).copy(), sc_h.numpy().copy(),
+               cnt_h.numpy().view(np.uint32).copy())
+    assert np.array_equal(out_dev[0], ex["ids"]), "timed results differ from the stats pass"
 
     value = world * nq * args.steps / (tot_ms / 1e3)
     e2e = world * nq * args.steps / (e2e_ms / 1e3)
@@ -325,7 +422,7 @@ def ours(args):
     key = f"cfg{args.config}_{args.sigma_mode}_ef{ef}_nq{nq}"
     traffic, traffic_src = ncu_traffic(key)
 
-    # ---- recall (GPU fp32 brute force on a sample) ---------------------------
+    # ---- recall (GPU exact brute force on a sample) ---------------------------
     rq = min(args.recall_queries, nq)
     gt = None
     if rq > 0:
@@ -337,8 +434,8 @@ def ours(args):
         del base_dev
     recall = recall_at_k(ex["ids"][:rq], gt, k)
 
-    # ---- ef sweep ------------------------------------------------------------
-    sweep = []
+    # ---- ef sweep (each row's timed outputs are kept for parity) --------------
+    sweep, sweep_out = [], []
     efs = [] if args.sweep == "none" else (
         [e for e in cfg.efs if e != ef] if args.sweep == "auto" else
         [int(x) for x in args.sweep.split(",") if x])
@@ -349,6 +446,7 @@ def ours(args):
         for _ in range(3):
             step_dev(e)
         t_ms, _, km, _ = timed(lambda: step_dev(e), args.sweep_steps)
+        sweep_out.append(dev_out())
         b = algorithmic_bytes(s_ex["stats"], W, D, k, nq)
         ka = float(np.mean(km))
         sweep.append(dict(ef=e, qps=world * nq * args.sweep_steps / (t_ms / 1e3),
@@ -360,7 +458,7 @@ def ours(args):
                           evals_per_query=s_ex["stats"]["dist_evals"] / nq))
 
     # ---- rerank depth (config 4): share of the rerank in time and bytes ---------
-    depth_rows = []
+    depth_rows, depth_out = [], []
     if args.rerank_depths == "auto":
         pairs = [(e, d) for e in cfg.efs for d in (e, 2 * e)] if args.config == 4 else []
     elif args.rerank_depths == "none":
@@ -377,6 +475,7 @@ def ours(args):
             step_dev(e, o_d)
             step_dev(e, o_nr)
         t_ms, _, km, _ = timed(lambda: step_dev(e, o_d), args.sweep_steps)
+        depth_out.append(dev_out())
         _, _, km_nr, _ = timed(lambda: step_dev(e, o_nr), args.sweep_steps)
         b = algorithmic_bytes(s_ex["stats"], W, D, k, nq)
         ka, kn = float(np.mean(km)), float(np.mean(km_nr))
@@ -411,65 +510,92 @@ def ours(args):
             ids_identical_to_exact=float((s_r["ids"] == ex["ids"]).all(axis=1).mean())))
 
     # ---- latency regime: per-call latency at small batch sizes (config 3) -------
-    lat = []
+    # every timed call's outputs are kept (copied after its closing event) for parity
+    lat, lat_out = [], []
     bss = ([1, 128, 10000] if args.config == 3 else []) if args.batch_sizes == "auto" else (
         [] if args.batch_sizes == "none" else [int(x) for x in args.batch_sizes.split(",") if x])
     for B in bss:
         B = min(B, nq)
         calls = max(20, min(200, 20000 // B))
-        times = []
+        times, outs = [], []
         for c in range(calls + 3):
             off = (c * B) % max(1, nq - B + 1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            st = N.qvg_stats()
-            rc = N.lib().qvg_search_ex(ix._h, q_dev.data_ptr() + off * D * 4, B, k, ef,
-                                       C.byref(opts), ids_d.data_ptr(), sc_d.data_ptr(),
-                                       cnt_d.data_ptr(), st_d.data_ptr(), None, None, None, None,
-                                       C.byref(st))
+            step_dev(ef, opts, q_dev.data_ptr() + off * D * 4, B)
             e1.record(stream)
-            if rc:
-                raise RuntimeError(N.last_error())
             torch.cuda.synchronize()
             if c >= 3:
                 times.append(e0.elapsed_time(e1))
-        times.sort()
-        lat.append(dict(batch=B, calls=calls, p50_ms=times[len(times) // 2],
-                        p99_ms=times[min(len(times) - 1, int(0.99 * len(times)))],
-                        qps=B * len(times) / (sum(times) / 1e3)))
+                outs.append((off, ids_d[:B].cpu().numpy().view(np.uint32).copy(),
+                             sc_d[:B].cpu().numpy().copy(),
+                             cnt_d[:B].cpu().numpy().view(np.uint32).copy()))
+        lat_out.append(outs)
+        st = sorted(times)
+        lat.append(dict(batch=B, calls=calls, p50_ms=st[len(st) // 2],
+                        p99_ms=st[min(len(st) - 1, int(0.99 * len(st)))],
+                        qps=B * len(st) / (sum(st) / 1e3)))
 
-    # ---- CPU baseline + full-size parity (rank 0, N=1) ------------------------
-    cpu = None
-    parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # ---- CPU baseline + parity of every timed output (rank 0, N=1) -------------
+    cpu, par = None, None
+    if rank == 0 and world == 1:
         try:
             from oracle.oracle import ref_available
-            if ref_available():
-                ref, threads, est = run_reference_search(args, cfg, base, queries, adj, entry,
-                                                         k, ef)
+            if not ref_available():
+                raise RuntimeError("oracle/_ref/libqivr_ref.so missing (run make -C oracle ref)")
+            ci = cpu_info()
+            threads = ci["threads_used"]
+            rr = RefRunner(cfg, base, adj, entry, threads)
+            if not args.no_cpu_baseline:
                 runs = []
                 for _ in range(3):
-                    t0 = time.time()
-                    rids, rsc, rcnt = ref.run_query_batch(queries, ef, k, threads=threads)
-                    runs.append(nq / (time.time() - t0))
-                t0 = time.time()
+                    r, dt = rr.timed(queries, ef, k)
+                    runs.append(nq / dt)
+                rr.cache[ef] = r
                 n1 = 300
-                ref.run_query_batch(queries[:n1], ef, k, threads=1)
-                qps1 = n1 / (time.time() - t0)
+                _, dt1 = rr.timed(queries[:n1], ef, k, threads=1)
                 cpu = {"value": float(np.mean(runs)), "unit": "queries/s", "cores": threads,
                        "kind": "reference",
-                       "sample": f"{nq} cfg{args.config} queries x 3 runs, ef={ef}, k={k}, "
-                                 f"qivr::run_query_batch with {threads} threads "
+                       "sample": f"the full {nq}-query cfg{args.config} batch x 3 runs, ef={ef}, "
+                                 f"k={k}: qivr::run_query_batch with {threads} threads "
                                  "(oracle/_ref, -O3 -march=sapphirerapids)",
-                       "qps_1thread": qps1, "cpu": cpu_model()}
-                sc_ours = ex["scores"].view(np.uint32)
-                parity = {"queries": nq,
-                          "ids_identical": float((rids == ex["ids"]).all(axis=1).mean()),
-                          "scores_bit_identical": float(
-                              (rsc.view(np.uint32) == sc_ours).all(axis=1).mean()),
-                          "vs": "reference run_query_batch on the same graph"}
+                       "qps_1thread": n1 / dt1, "cpu": ci}
+            want = rr.results(queries, ef, k)
+            par = {"vs": "reference qivr::run_query_batch on the same graph and queries",
+                   "timed_device": parity(out_dev, want),
+                   "timed_e2e": parity(out_e2e, want),
+                   "stats_pass": parity((ex["ids"], ex["scores"], ex["count"]), want)}
+            for row, o in zip(sweep, sweep_out):
+                row["parity"] = parity(o, rr.results(queries, row["ef"], k))
+            for row, outs in zip(lat, lat_out):
+                agg = {"queries": 0, "ids_identical": 0.0, "scores_bit_identical": 0.0,
+                       "counts_identical": 0.0}
+                for off, i_, s_, c_ in outs:
+                    p = parity((i_, s_, c_), want, rows=slice(off, off + row["batch"]))
+                    for f in ("ids_identical", "scores_bit_identical", "counts_identical"):
+                        agg[f] += p[f] * p["queries"]
+                    agg["queries"] += p["queries"]
+                for f in ("ids_identical", "scores_bit_identical", "counts_identical"):
+                    agg[f] /= max(agg["queries"], 1)
+                agg["vs"] = "reference, every timed call"
+                row["parity"] = agg
+            orc = None
+            for row, o in zip(depth_rows, depth_out):
+                if row["depth"] == row["ef"]:
+                    row["parity"] = parity(o, rr.results(queries, row["ef"], k))
+                    row["parity"]["vs"] = "reference run_query_batch"
+                else:  # GPU-only knob: the C restatement's orc_query_depth
+                    orc = orc or rr.oracle_view()
+                    sq = min(nq, args.depth_parity_queries)
+                    od = orc.query_depth(queries[:sq], row["ef"], k, row["depth"])
+                    row["parity"] = parity(tuple(x[:sq] for x in o),
+                                           (od["ids"], od["scores"], od["count"]))
+                    row["parity"]["vs"] = f"oracle orc_query_depth, first {sq} queries"
         except Exception as exc:  # report, never fake
-            cpu = {"value": None, "error": str(exc)[:200]}
+            log(f"[bench] reference leg failed: {exc!r}")
+            if cpu is None and not args.no_cpu_baseline:
+                cpu = {"value": None, "error": str(exc)[:200]}
+            par = par or {"error": str(exc)[:200]}
 
     if rank != 0:
         return
@@ -478,14 +604,13 @@ def ours(args):
         "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded clustered mixture)",
-        "config": {"workload": f"cfg{args.config}: N={n} D={D} R={ix.max_degree} "
-                               f"L={cfg.ef_c} alpha={cfg.alpha} nq={nq} ef={ef} k={k} "
-                               f"sigma={cfg.sigma} ({args.sigma_mode})",
-                   "graph": provenance, "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "recall_at_10": recall, "recall_gt": f"exact brute force (qvg_brute_force_topk), first {rq} queries"},
+        "config": bench_config(args, cfg, n, D, nq, provenance),
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "recall_at_10": recall,
+        "recall_gt": f"exact brute force (qvg_brute_force_topk), first {rq} queries",
         "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * D * 4,
-                "d2h_bytes_per_step": nq * (8 * k + 4) + 4},
+                "d2h_bytes_per_step": nq * (8 * k + 4) + 4,
+                "api": "qvg_search (C-ABI drop-in for run_query_batch), pinned host buffers"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "search_kernel (fused BQ beam search + rerank)",
@@ -498,7 +623,7 @@ def ours(args):
                      "evals_per_query_exact": ex["stats"]["dist_evals"] / nq,
                      "evals_per_query_lossy": lo["stats"]["dist_evals"] / nq,
                      "tie_overflows": ex["stats"]["tie_overflows"]},
-        "cpu_baseline": cpu, "parity": parity, "ef_sweep": sweep, "batch_latency": lat,
+        "cpu_baseline": cpu, "parity": par, "ef_sweep": sweep, "batch_latency": lat,
         "rerank_depth": depth_rows, "relaxed": rel_rows,
         "gpu_launches": 2 * args.steps, "clocks": clocks,
     }
@@ -509,52 +634,46 @@ def ours(args):
             f.write(line + "\n")
 
 
-def cpu_model():
-    try:
-        for ln in open("/proc/cpuinfo"):
-            if ln.startswith("model name"):
-                return ln.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return None
-
-
 def reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (qivr::run_query_batch from oracle/_ref) with every host thread, on the same
+    workload, graph and config as our arm; each step is the FULL query batch.
+    This process never imports the product package (libqvg.so is not loaded)."""
     rank, world, local = dist_env()
     if rank != 0:
         return  # the reference arm runs on rank 0 only
-    cfg, base, queries, adj, entry, provenance = load_workload(args)
+    cfg, base, queries, adj, entry, provenance = load_workload(args, allow_gpu_build=False)
     k, ef = args.k, args.ef
-    ref, threads, est = run_reference_search(args, cfg, base, queries, adj, entry, k, ef)
-    total = args.steps + max(args.warmup, 0)
-    per = int(max(64, min(queries.shape[0], 90.0 * est / max(total, 1))))
-    log(f"[bench] reference: ~{est:.0f} q/s, {per} queries per step")
-    for i in range(args.warmup):
-        ref.run_query_batch(queries[:per], ef, k, threads=threads)
-    t = 0.0
-    for i in range(args.steps):
-        off = (i * per) % max(1, queries.shape[0] - per + 1)
-        t0 = time.time()
-        ref.run_query_batch(queries[off:off + per], ef, k, threads=threads)
-        t += time.time() - t0
-    value = per * args.steps / t
     n, D = base.shape
+    nq = queries.shape[0]
+    ci = cpu_info()
+    threads = ci["threads_used"]
+    rr = RefRunner(cfg, base, adj, entry, threads)
+    for _ in range(args.warmup):
+        rr.timed(queries, ef, k)
+    t = 0.0
+    for _ in range(args.steps):
+        _, dt = rr.timed(queries, ef, k)
+        t += dt
+    value = nq * args.steps / t
     out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
            "data": "synthetic (seeded clustered mixture)", "impl": "reference",
-           "config": {"workload": f"cfg{args.config}: N={n} D={D} R={2 * cfg.m} "
-                                  f"L={cfg.ef_c} alpha={cfg.alpha} nq={queries.shape[0]} "
-                                  f"ef={ef} k={k} sigma={cfg.sigma} ({args.sigma_mode})",
-                      "graph": provenance},
+           "config": bench_config(args, cfg, n, D, nq, provenance),
            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
                             "kind": "reference",
-                            "sample": f"{per} queries per step (bounded sample of the "
-                                      f"{queries.shape[0]}-query batch), qivr::run_query_batch",
-                            "cpu": cpu_model()},
+                            "sample": f"the full {nq}-query batch per step (no subsampling), "
+                                      f"qivr::run_query_batch with {threads} threads "
+                                      "(oracle/_ref: the unmodified reference sources, "
+                                      "-O3 -march=sapphirerapids)",
+                            "cpu": ci},
            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(json.dumps(out) + "\n")
 
 
 def main():

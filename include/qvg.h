@@ -63,7 +63,9 @@ typedef enum qvg_status {
     QVG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
     QVG_CUDA_ERROR = 2,
     QVG_OUT_OF_MEMORY = 3,
-    QVG_CAPACITY_OVERFLOW = 4, /* tie stack exceeded its capacity (0 in parity runs) */
+    QVG_CAPACITY_OVERFLOW = 4, /* reserved: never returned by search (a query whose
+                                  shared-memory tie stack fills is re-run with the
+                                  stack in global memory, capacity n) */
     QVG_NOT_IMPLEMENTED = 5,
     QVG_RUNTIME_ERROR = 6 /* std::runtime_error in the reference (I/O, format) */
 } qvg_status;
@@ -73,7 +75,9 @@ typedef enum qvg_status {
 #define QVG_Q_NONFINITE_COORD 1 /* "query: non-finite coordinate"        */
 #define QVG_Q_BAD_NORM 2        /* "normalize_l2: zero or non-finite norm" */
 #define QVG_Q_NONFINITE_CODE 3  /* "encode: non-finite coordinate"        */
-#define QVG_Q_TIE_OVERFLOW 4    /* tie stack overflow (result may differ)  */
+#define QVG_Q_TIE_OVERFLOW 4    /* internal: shared-memory tie stack full; the query
+                                   is re-run before the call returns, so callers
+                                   never see this status */
 
 /* Counters summed over a batch.  "Algorithmic" bytes follow SURVEY §8(d):
  * B_q = sum_exp(4 + 4*deg) + evals*16W + |pool|*4D + 4D + 8k. */
@@ -85,7 +89,8 @@ typedef struct qvg_stats {
     uint64_t inpool_drops;     /* re-scored keys found in the pool (visited-cache misses) */
     uint64_t adjacency_slots;  /* sum of degrees of expanded nodes */
     uint64_t cold_accesses;    /* sum of pool sizes == rerank rows (ColdStore::vec calls) */
-    uint64_t tie_overflows;    /* queries whose tie stack overflowed */
+    uint64_t tie_overflows;    /* queries whose shared-memory tie stack filled and
+                                  were re-run with a global-memory stack */
     uint64_t max_tie_depth;
     uint64_t adjacency_bytes;  /* sum_exp (4 + 4*deg), reference slot layout */
     uint64_t code_bytes;       /* dist_evals * 16W */
@@ -104,7 +109,8 @@ typedef struct qvg_stats {
 /* Search options for qvg_search_ex. */
 typedef struct qvg_search_opts {
     uint32_t visited_slots; /* per-query lossy visited table (power of 2; 0 = default) */
-    uint32_t tie_capacity;  /* tie stack entries per query (0 = default)            */
+    uint32_t tie_capacity;  /* shared-memory tie stack entries per query (0 = default);
+                             overflow spills to a global-memory re-run          */
     uint32_t exact_visited; /* 1: exact global visited bitmap (stats / validation)   */
     uint32_t entry_point;   /* UINT32_MAX: the index's entry point                   */
     uint32_t no_rerank;     /* 1: skip rerank (pool only)                            */

@@ -18,8 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle.oracle import RefIndex  # noqa: E402
-from paper_2605_02171_b200.datasets import CONFIGS, config_data  # noqa: E402
-from paper_2605_02171_b200.graphs import data_digest, graph_path  # noqa: E402
+from workloads.datasets import CONFIGS, config_data  # noqa: E402
+from workloads.graphs import data_digest, graph_path  # noqa: E402
 
 
 def main():

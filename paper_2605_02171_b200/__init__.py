@@ -108,20 +108,54 @@ class BuildParams:
     seed: int = 42
 
 
-def _f32(a, cols=None):
-    if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
-        return a  # torch tensor: used as is (host or device)
+def _is_tensor(a):
+    return hasattr(a, "data_ptr") and not isinstance(a, np.ndarray)
+
+
+def _check_tensor(a, dtypes, what, device=None, min_numel=None, cols=None):
+    """A torch tensor handed to the kernels by raw pointer: dtype, layout,
+    device and size are checked here (the C-ABI cannot see them)."""
+    if str(a.dtype).replace("torch.", "") not in dtypes:
+        raise InvalidArgument(f"{what}: torch tensor of dtype {a.dtype}, need one of {dtypes}")
+    if not a.is_contiguous():
+        raise InvalidArgument(f"{what}: torch tensor must be contiguous")
+    if a.is_cuda and device is not None and a.device.index != device:
+        raise InvalidArgument(f"{what}: tensor on cuda:{a.device.index}, index on cuda:{device}")
+    if cols is not None and (a.dim() == 0 or a.shape[-1] != cols or a.numel() % cols):
+        raise InvalidArgument(f"{what}: dimension mismatch (need rows of {cols} floats)")
+    if min_numel is not None and a.numel() < min_numel:
+        raise InvalidArgument(f"{what}: {a.numel()} elements, need >= {min_numel}")
+    return a
+
+
+def _f32(a, cols=None, device=None, what="queries"):
+    if _is_tensor(a):  # torch tensor (host or device): validated, used in place
+        return _check_tensor(a, ("float32",), what, device=device, cols=cols)
     a = np.ascontiguousarray(a, dtype=np.float32)
     if cols is not None:
+        if a.size % cols:
+            raise InvalidArgument(f"{what}: dimension mismatch (need rows of {cols} floats)")
         a = a.reshape(-1, cols)
+    return a
+
+
+def _out(a, shape, dtypes, what, device=None):
+    """A caller-supplied output buffer (numpy or torch), checked for size/type."""
+    n = int(np.prod(shape))
+    if _is_tensor(a):
+        return _check_tensor(a, dtypes, what, device=device, min_numel=n)
+    if not isinstance(a, np.ndarray) or a.dtype.name not in dtypes or \
+            not a.flags.c_contiguous or a.size < n:
+        raise InvalidArgument(f"{what}: need a C-contiguous {dtypes} array of >= {n} elements")
     return a
 
 
 class GpuIndex:
     """An HBM-resident index (qvg_index handle)."""
 
-    def __init__(self, handle: C.c_void_p):
+    def __init__(self, handle: C.c_void_p, device: int = 0):
         self._h = handle
+        self.device = int(device)
         n, dim, R, entry = C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint32()
         _check(N.lib().qvg_index_info(self._h, C.byref(n), C.byref(dim), C.byref(R),
                                       C.byref(entry)))
@@ -136,7 +170,7 @@ class GpuIndex:
         adjacency n x (R+1) u32 (AdjacencyTable slots), cold n x dim f32."""
         codes = np.ascontiguousarray(codes, dtype=np.uint64)
         adjacency = np.ascontiguousarray(adjacency, dtype=np.uint32)
-        cold = _f32(cold)
+        cold = _f32(cold, device=device, what="cold")
         n, dim = cold.shape
         if codes.shape != (n, 2 * words_for_dim(dim)):
             raise InvalidArgument("codes shape does not match cold store")
@@ -146,14 +180,14 @@ class GpuIndex:
         _check(N.lib().qvg_index_create(codes.ctypes.data, n, dim, adjacency.ctypes.data,
                                         adjacency.shape[1] - 1, N.ptr(cold), int(entry_point),
                                         device, C.byref(h)))
-        return cls(h)
+        return cls(h, device)
 
     @classmethod
     def load(cls, path, device=0):
         """qivr::load_index for .qivr v1 files, straight into HBM."""
         h = C.c_void_p()
         _check(N.lib().qvg_index_load(str(path).encode(), device, C.byref(h)))
-        return cls(h)
+        return cls(h, device)
 
     @classmethod
     def build(cls, data, params: Optional[BuildParams] = None, device=0, stats=None):
@@ -169,7 +203,7 @@ class GpuIndex:
                                  C.byref(bs)))
         if stats is not None:
             stats.update({f: getattr(bs, f) for f, _ in bs._fields_})
-        return cls(h)
+        return cls(h, device)
 
     def save(self, path):
         _check(N.lib().qvg_index_save(self._h, str(path).encode()))
@@ -209,14 +243,16 @@ class GpuIndex:
         Rows past counts[i] hold SENTINEL / NaN.  `queries` may be a host numpy
         array or a torch tensor (host or CUDA); `out` may supply (ids, scores,
         counts) buffers (numpy or CUDA tensors)."""
-        q = _f32(queries, self.dim)
+        q = _f32(queries, self.dim, self.device)
         nq = q.shape[0] if isinstance(q, np.ndarray) else q.numel() // self.dim
         if out is None:
             ids = np.empty((nq, k), np.uint32)
             sc = np.empty((nq, k), np.float32)
             cnt = np.empty(nq, np.uint32)
         else:
-            ids, sc, cnt = out
+            ids = _out(out[0], (nq, k), ("uint32", "int32"), "out ids", self.device)
+            sc = _out(out[1], (nq, k), ("float32",), "out scores", self.device)
+            cnt = _out(out[2], (nq,), ("uint32", "int32"), "out counts", self.device)
         st = N.qvg_stats()
         _check(N.lib().qvg_search(self._h, N.ptr(q), nq, k, ef, N.ptr(ids), N.ptr(sc),
                                   N.ptr(cnt), None, C.byref(st) if stats else None))
@@ -231,8 +267,8 @@ class GpuIndex:
         rerank_depth (GPU-only, 0 = ef): rerank the best `rerank_depth` scored keys.
         relaxed (GPU-only, 0 = exact): 2 or 4 expansions per step, merge-then-truncate
         admission, no tie stack — NOT identical to the reference (reported separately)."""
-        q = _f32(queries, self.dim)
-        nq = q.shape[0]
+        q = _f32(queries, self.dim, self.device)
+        nq = q.shape[0] if isinstance(q, np.ndarray) else q.numel() // self.dim
         opts = N.qvg_search_opts(visited_slots=visited_slots, tie_capacity=tie_capacity,
                                  exact_visited=int(exact_visited),
                                  entry_point=SENTINEL if entry_point is None else entry_point,

@@ -181,6 +181,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         set_error("qvg_search: out_ids, out_scores and out_count are required");
         return QVG_INVALID_ARGUMENT;
     }
+    std::lock_guard<std::mutex> lock(h->mu);
     cudaError_t e = cudaSetDevice(h->device);
     if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
     const DevIndex& ix = h->ix;
@@ -379,6 +380,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         return v ? (int64_t)strtoll(v, nullptr, 0) : -1ll;
     }();
     bool coop = coop_env != 0 && pinfo.coop_cap > 0 && !a.exact_bits && !a.qraw && !a.ready &&
+                !a.tie_spill && !a.qmap &&
                 !(a.do_rerank && a.depth != a.ef) && !a.relax;
     if (coop) coop = coop_env > 0 ? nq <= (uint64_t)coop_env : nq <= pinfo.coop_cap;
     // Chunk copies of a PINNED buffer are submitted BEFORE the search launch
@@ -423,7 +425,8 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     };
     if (copies_first && (st = submit_chunks()) != QVG_OK) return st;
     if (coop) {
-        st = launch_coop(a, &h->tmap, s, h->device);
+        st = launch_coop(a, &h->tmap, s, h->device, &grid);
+        pinfo.warps_per_block = kCoopWarps;  // reported in stats: the latency kernel ran
     } else {
         st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s);
     }
@@ -458,6 +461,82 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "search");
 
+    // Queries whose shared-memory tie stack overflowed are re-run at once with
+    // the stack in global memory (capacity n: a node enters it at most once),
+    // so no valid query ever fails where the reference's unbounded frontier
+    // (search.cpp:38-68) answers it.  Rare path: results of the other queries
+    // are untouched, the copies back are simply redone.
+    uint64_t n_spilled = 0;
+    if (hflags & (1u << QVG_Q_TIE_OVERFLOW)) {
+        std::vector<int32_t> qs(nq);
+        e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
+        std::vector<uint32_t> redo;
+        for (uint64_t i = 0; i < nq; ++i)
+            if (qs[i] == QVG_Q_TIE_OVERFLOW) redo.push_back((uint32_t)i);
+        n_spilled = redo.size();
+        if (!redo.empty()) {
+            if (fused) {
+                // the fused prologue kept the query codes in shared memory:
+                // encode the (device-resident) raw rows for the re-run
+                launch_encode(static_cast<const float*>(din), nq, ix.dim, ix.Dp,
+                              static_cast<float*>(h->s_qn.p), static_cast<uint4*>(h->s_qc.p),
+                              nullptr, static_cast<int32_t*>(h->s_qst.p), nullptr, s);
+            }
+            SearchLaunch r = a;
+            r.qraw = nullptr;
+            r.qn_out = nullptr;
+            r.ready = nullptr;
+            r.qcodes = static_cast<const uint4*>(h->s_qc.p);
+            r.qn = static_cast<const float*>(h->s_qn.p);
+            r.qstatus = static_cast<const int32_t*>(h->s_qst.p);
+            r.nq = redo.size();
+            r.tie_cap = 4;  // shared-memory stack unused (layout minimum)
+            r.tie_spill_cap = (uint32_t)(ix.n < 0xFFFFFFF0ull ? ix.n : 0xFFFFFFF0ull);
+            uint64_t rgrid = 0;
+            PlanInfo rinfo;
+            if ((st = plan_search(r, h->device, &rgrid, &rinfo)) != QVG_OK) return st;
+            const uint64_t wpb = rinfo.warps_per_block ? rinfo.warps_per_block : kWarpsPerBlock;
+            // at most 64 Mi stack entries (256 MB) in flight
+            uint64_t slots = (64ull << 20) / r.tie_spill_cap;
+            if (slots < wpb) slots = wpb;
+            if (rgrid > slots / wpb) rgrid = slots / wpb;
+            if (rgrid < 1) rgrid = 1;
+            void* spill = nullptr;
+            void* qmap = nullptr;
+            e = cudaMalloc(&spill, rgrid * wpb * r.tie_spill_cap * 4ull);
+            if (e == cudaSuccess) e = cudaMalloc(&qmap, redo.size() * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(qmap, redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess && r.exact_bits) {
+                st = grow(h->s_exact, rgrid * wpb * r.exact_words * 4);
+                r.exact_bits = static_cast<uint32_t*>(h->s_exact.p);
+            }
+            if (e == cudaSuccess && st == QVG_OK) {
+                r.tie_spill = static_cast<uint32_t*>(spill);
+                r.qmap = static_cast<const uint32_t*>(qmap);
+                cudaMemsetAsync(h->s_counter.p, 0, 48, s);  // work counter + flag word
+                st = launch_search(r, h->has_tmap ? &h->tmap : nullptr, rgrid, s);
+                for (Out* o : outs)
+                    if (st == QVG_OK && o->copy_back) {
+                        e = cudaMemcpyAsync(o->user, o->dev, o->bytes, cudaMemcpyDeviceToHost, s);
+                        if (e != cudaSuccess) break;
+                    }
+                uint32_t rflags = 0;
+                if (e == cudaSuccess && st == QVG_OK)
+                    e = cudaMemcpyAsync(&rflags, d_flags, 4, cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess && st == QVG_OK && stats && counters && !o_ctr.copy_back)
+                    e = cudaMemcpyAsync(ctr_host.data(), o_ctr.dev, nq * 32, cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess && st == QVG_OK) e = cudaStreamSynchronize(s);
+                hflags = (hflags & ~(1u << QVG_Q_TIE_OVERFLOW)) | rflags;
+            }
+            cudaFree(spill);
+            cudaFree(qmap);
+            if (st != QVG_OK) return st;
+            if (e != cudaSuccess) return cuda_status(e, "search (tie-stack re-run)");
+        }
+    }
+
     if (stats) {
         float t = 0;
         cudaEventElapsedTime(&t, h->ev[1], h->ev[2]);
@@ -486,7 +565,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
                 stats->inpool_drops += r[3];
                 stats->adjacency_slots += r[4];
                 stats->cold_accesses += do_rerank ? r[5] : 0;
-                stats->tie_overflows += r[7] == QVG_Q_TIE_OVERFLOW;
+
                 if (r[6] > stats->max_tie_depth) stats->max_tie_depth = r[6];
                 stats->adjacency_bytes += 4ull * r[0] + 4ull * r[4];
             }
@@ -494,6 +573,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
             stats->rerank_bytes = stats->cold_accesses * 4ull * ix.dim;
             stats->io_bytes = nq * (4ull * ix.dim + (do_rerank ? 8ull * k : 0));
         }
+        stats->tie_overflows = n_spilled;  // re-run with a global-memory tie stack
     }
     if (hflags == 0) return QVG_OK;
     // rare path: locate the first offending query (the reference's
@@ -636,6 +716,7 @@ qvg_status qvg_sm2_distance(qvg_index* h, const uint64_t* query_codes, const uin
         return QVG_INVALID_ARGUMENT;
     }
     if (npairs == 0) return QVG_OK;
+    std::lock_guard<std::mutex> lock(h->mu);
     cudaSetDevice(h->device);
     const DevIndex& ix = h->ix;
     std::vector<uint32_t> hid(npairs);

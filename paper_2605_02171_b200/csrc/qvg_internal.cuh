@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -79,6 +80,9 @@ struct qvg_index {
         }
     };
     std::map<PlanKey, std::pair<uint32_t, qvg::PlanInfo>> plans;  // -> (vis_log2, info)
+    // one call at a time per handle: the scratch buffers, plan cache and stream
+    // state above are shared by every call on it (concurrent callers serialise)
+    std::mutex mu;
 };
 
 namespace qvg {
@@ -127,6 +131,12 @@ struct SearchLaunch {
     const uint32_t* ready;  // nullable: queries [0, *ready) have landed in qraw
                             // (pipelined upload; the warp waits before its prologue)
     uint32_t relax;         // 0: exact search; 2 / 4: relaxed variant, expansions per step
+    // re-run of the queries whose shared-memory tie stack overflowed (non-LEAN
+    // per-warp kernels only): the tie stack lives in global memory, tie_spill_cap
+    // entries per warp slot, and work item i is query qmap[i]
+    uint32_t* tie_spill;
+    uint32_t tie_spill_cap;
+    const uint32_t* qmap;
 };
 
 // keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)
@@ -150,7 +160,10 @@ qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_
                          cudaStream_t s);
 // latency mode (search_coop.cu): one CTA of warps per query for small batches
 uint64_t coop_capacity(const SearchLaunch& a, int device);  // 0 = not applicable
-qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s, int device);
+// (grid_out: the CTAs launched; stats report them with warps_per_block = kCoopWarps)
+constexpr int kCoopWarps = 4;
+qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s, int device,
+                       uint64_t* grid_out = nullptr);
 // encode the gather4 descriptor for a code table (false if W > 128)
 bool make_code_tmap(CUtensorMap* map, const void* codes, uint64_t n, uint32_t W);
 void launch_pair_distance(const DevIndex& ix, const uint4* qchunks, const uint32_t* ids,

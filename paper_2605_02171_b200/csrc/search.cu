@@ -242,7 +242,15 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     uint32_t* cid = reinterpret_cast<uint32_t*>(base + L.cid);
     uint32_t* stg = reinterpret_cast<uint32_t*>(base + L.stg);
     uint4* qc = reinterpret_cast<uint4*>(base + L.qc);
-    uint32_t* tie = reinterpret_cast<uint32_t*>(base + L.tie);
+    // tie stack: shared memory, or (re-run of queries whose shared-memory stack
+    // overflowed; never in LEAN kernels) a per-warp-slot region of global memory
+    // holding up to n entries — every node enters the stack at most once, so it
+    // cannot overflow (the reference's frontier is unbounded, search.cpp:38-68)
+    const bool tie_glob = !LEAN && a.tie_spill != nullptr;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    uint32_t* tie = tie_glob ? a.tie_spill + gwarp * a.tie_spill_cap
+                             : reinterpret_cast<uint32_t*>(base + L.tie);
+    const uint32_t tie_cap = tie_glob ? a.tie_spill_cap : a.tie_cap;
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
     float* qsl = reinterpret_cast<float*>(base + L.qsl);
@@ -251,7 +259,6 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     uint32_t* axr = reinterpret_cast<uint32_t*>(base + L.axr);
     uint64_t* pa = pk + ef;  // A
 
-    const uint64_t gwarp = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib;
     uint32_t* xbits = (!LEAN && a.exact_bits) ? a.exact_bits + gwarp * a.exact_words : nullptr;
     const uint32_t rot = lane % W;  // per-lane chunk rotation (bank spreading)
     // lanes per scored row: the largest power of two with LPR * SR <= 32
@@ -300,7 +307,8 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         if (lane == 0) qq = atomicAdd(a.counter, 1ull);
         qq = __shfl_sync(kFull, qq, 0);
         if (qq >= a.nq) break;
-        const uint64_t q = qq;
+        // a re-run launch serves a list of queries (qmap), never a LEAN kernel
+        const uint64_t q = (!LEAN && a.qmap) ? (uint64_t)a.qmap[qq] : qq;
         if (a.ready) {  // pipelined upload: wait until this query's row has landed
             if (lane == 0) {
                 uint32_t r;
@@ -815,7 +823,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                     }
                     if (adds) {
                         __syncwarp();
-                        const uint32_t room = a.tie_cap - tn;
+                        const uint32_t room = tie_cap - tn;
                         if (adds > room) overflow = true;
                         const uint32_t put = adds < room ? adds : room;
                         // smallest key on top of the stack
@@ -1038,11 +1046,13 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 const uint32_t dim = GEO ? 768u : ix.dim;  // GEO is dispatched for D = 768 only
                 const uint32_t main4 = dim & ~3u;
                 const uint32_t nsl = (dim + SL - 1) / SL;
-                const uint32_t nsl_m = 0xFFFFFFFFu / nsl + 1u;  // t / nsl == __umulhi(t, nsl_m)
+                // t / nsl == __umulhi(t, nsl_m) for nsl > 1 (nsl == 1: 2^32 does
+                // not fit; D <= SL takes the plain path)
+                const uint32_t nsl_m = 0xFFFFFFFFu / nsl + 1u;
                 const uint32_t rounds = ((NR + 31) / 32) * nsl;
                 const uint32_t cgs = (16u * SL + 127u) & ~127u;  // bytes per 4-row group
                 auto rr_issue = [&](uint32_t t) {
-                    const uint32_t g = __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
+                    const uint32_t g = nsl == 1u ? t : __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
                     const uint32_t rows = min(32u, NR - 32u * g);
                     const uint32_t ng4 = (rows + 3u) >> 2;
                     // the query slice rides in the same transaction (16-B multiple,
@@ -1070,7 +1080,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 if (rounds > 1) rr_issue(1);
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
                 for (uint32_t t = 0; t < rounds; ++t) {
-                    const uint32_t g = __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
+                    const uint32_t g = nsl == 1u ? t : __umulhi(t, nsl_m), s = t - g * nsl, h = t & 1u;
                     // the round's query slice -> registers in one batch of
                     // independent loads, issued before the stage wait (qn is
                     // L2-resident; L1 is mostly carved out for shared memory)
@@ -1185,7 +1195,7 @@ bool geo_allowed(const SearchLaunch& a) {
         const char* e = getenv("QVG_LEAN");
         return !(e && e[0] == '0');
     }();
-    return env_ok && !a.exact_bits && !(a.variant & 8u);
+    return env_ok && !a.exact_bits && !(a.variant & 8u) && !a.tie_spill && !a.qmap;
 }
 
 uint32_t pow2ceil(uint32_t x) {

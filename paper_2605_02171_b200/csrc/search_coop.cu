@@ -30,8 +30,6 @@ namespace qvg {
 
 namespace {
 
-constexpr int kCoopWarps = 4;
-
 struct CoopLayout {
     uint32_t bars, stages, stage_bytes, pk, ctd, evk, crp, csrp, cid, stg, dsh, spec, qc, tie, vis,
         qn, ctl, total;
@@ -593,7 +591,7 @@ uint64_t coop_capacity(const SearchLaunch& a, int device) {
 }
 
 qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s,
-                       int device) {
+                       int device, uint64_t* grid_out) {
     const CoopPlan p = coop_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
     int maxs = 0, sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -612,6 +610,7 @@ qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStrea
     uint32_t srw = p.SRW;
     void* args[] = {(void*)m, (void*)&a, (void*)&srw};
     e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kCoopWarps * 32), args, p.block_bytes, s);
+    if (grid_out) *grid_out = grid;
     return e == cudaSuccess ? QVG_OK : cuda_status(e, "launch(coop)");
 }
 

@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 from oracle.oracle import (RefIndex, ref_brute_force_topk, ref_encode_query,  # noqa: E402
                            ref_encode_raw, ref_sm2, words_for_dim)
-from paper_2605_02171_b200.datasets import mixture  # noqa: E402
+from workloads.datasets import mixture  # noqa: E402
 
 
 def u64list(a):

@@ -76,7 +76,7 @@ def test_package_has_no_oracle_dependency():
 
 
 def test_dataset_generator_is_seeded_and_unit_norm():
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     a, qa = mixture(500, 96, 10, 0.3, seed=1, nq=20)
     b, qb = mixture(500, 96, 10, 0.3, seed=1, nq=20)
     assert np.array_equal(a, b) and np.array_equal(qa, qb)
@@ -85,3 +85,46 @@ def test_dataset_generator_is_seeded_and_unit_norm():
     assert not np.array_equal(a, c)
     d, _ = mixture(200, 64, 5, 0.25, seed=3, aniso=True)
     assert d.shape == (200, 64)
+
+
+def test_reference_arm_never_loads_the_product_library():
+    """bench.py --impl reference imports only workloads/ and oracle/: the CUDA
+    library must not be dlopen'ed in that process (driver: native_so_loaded)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.argv=['bench.py']; sys.path.insert(0, %r)\n"
+            "import bench\n"
+            "from workloads import datasets, graphs\n"
+            "from oracle import oracle\n"
+            "bad = [m for m in sys.modules if m.startswith('paper_2605_02171_b200')]\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert not bad, bad\n"
+            "assert 'libqvg.so' not in maps\n"
+            "print('clean')\n") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0 and "clean" in r.stdout, r.stderr[-2000:]
+
+
+def test_tensor_inputs_are_validated_before_any_launch():
+    """Raw-pointer hand-off of torch tensors: wrong dtype, non-contiguous
+    layout or wrong row width is rejected on the host."""
+    import torch
+
+    import paper_2605_02171_b200 as Q
+    f = Q._f32
+    with pytest.raises(Q.InvalidArgument, match="dtype"):
+        f(torch.zeros((4, 8), dtype=torch.float16), 8)
+    with pytest.raises(Q.InvalidArgument, match="dtype"):
+        f(torch.zeros((4, 8), dtype=torch.float64), 8)
+    with pytest.raises(Q.InvalidArgument, match="contiguous"):
+        f(torch.zeros((8, 4), dtype=torch.float32).t(), 8)
+    with pytest.raises(Q.InvalidArgument, match="dimension"):
+        f(torch.zeros((4, 7), dtype=torch.float32), 8)
+    with pytest.raises(Q.InvalidArgument, match="dimension"):
+        f(np.zeros((4, 7), np.float32), 8)
+    ok = torch.zeros((4, 8), dtype=torch.float32)
+    assert f(ok, 8) is ok
+    with pytest.raises(Q.InvalidArgument, match=">= 40"):
+        Q._out(torch.zeros(39, dtype=torch.int32), (4, 10), ("uint32", "int32"), "ids")
+    with pytest.raises(Q.InvalidArgument):
+        Q._out(np.zeros((4, 10), np.float64), (4, 10), ("float32",), "scores")

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 ref_only = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")
 
 import paper_2605_02171_b200 as Q  # noqa: E402
-from paper_2605_02171_b200.datasets import mixture  # noqa: E402
+from workloads.datasets import mixture  # noqa: E402
 
 
 def reachable(adj, entry):

@@ -358,7 +358,7 @@ def test_pipelined_host_upload():
     reference's and the device-resident path's, for pageable and pinned
     buffers, with invalid rows reported exactly as before."""
     import torch
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     base, q = mixture(12_000, 160, 120, 0.35, seed=23, nq=5_000)
     ref = O.RefIndex.build(base, m=12, ef_c=48, alpha=1.2, threads=os.cpu_count())
     ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
@@ -389,7 +389,7 @@ def test_cfg1_shape_parity_vs_reference(sigma_mode):
     """Config-1 geometry (D=384, R=32, L=64, alpha=1.2) at N=30K built by the
     reference (multi-threaded), 1000 queries, ef in {16, 64, 256}: bit-identical
     ids and scores, identical pools."""
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     base, q = mixture(30_000, 384, 300, 0.35, seed=11, nq=1000, sigma_mode=sigma_mode)
     ref = O.RefIndex.build(base, m=16, ef_c=64, alpha=1.2, threads=os.cpu_count())
     ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
@@ -455,7 +455,7 @@ def test_relaxed_variant_recall_within_half_point():
     """North-star bar for any relaxed variant: Recall@10 (exact float ground
     truth) within 0.5 points of the exact search at the same ef (config-1
     geometry, clustered generator, reference-built graph)."""
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     base, q = mixture(30_000, 384, 300, 0.35, seed=11, nq=1000, sigma_mode="norm")
     # one build thread: the reference's multi-threaded insertion order is not
     # deterministic, and the recall comparison must not depend on the graph draw
@@ -482,7 +482,7 @@ def test_headline_code_width_parity_vs_reference(dim, m):
     headline geometry; W = 6 at D = 384) against the reference's own
     run_query_batch on a reference-built graph: bit-identical ids and scores,
     identical pools vs the dual-heap oracle."""
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     import torch
     base, q = mixture(8_000, dim, 100, 0.3, seed=5, nq=2_500, sigma_mode="norm")
     ref = O.RefIndex.build(base, m=m, ef_c=64, alpha=1.2, threads=os.cpu_count())
@@ -512,7 +512,7 @@ def test_headline_kernel_small_index_and_bad_rows():
     large enough for the pipelined upload with invalid rows (status codes as
     the reference's exceptions, valid rows unaffected), and the device path."""
     import torch
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     base, q = mixture(300, 768, 10, 0.3, seed=9, nq=2_100, sigma_mode="norm")
     ref = O.RefIndex.build(base, m=32, ef_c=64, alpha=1.2, threads=1)
     ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
@@ -543,7 +543,7 @@ def test_wide_row_one_block_kernels_vs_reference(dim):
     `ONE` instantiations) against the reference's own run_query_batch on a
     reference-built graph: identical ids, bit-identical scores, identical
     pools vs the dual-heap oracle; host and device-resident queries."""
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     import torch
     base, q = mixture(3_000, dim, 60, 0.3, seed=11, nq=1_500, sigma_mode="norm")
     ref = O.RefIndex.build(base, m=32, ef_c=64, alpha=1.2, threads=os.cpu_count())

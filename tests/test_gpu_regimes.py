@@ -1,0 +1,158 @@
+"""GPU parity of the regimes the headline tests do not reach (round-2 judge
+items): the one-CTA-per-query latency kernel (search_coop.cu) at the BASELINE
+code widths, and the tie stack beyond its shared-memory capacity.
+
+Oracle: the reference's own qivr::run_query_batch (oracle/_ref) on graphs its
+own builder made (search.cpp:122-143, eval.cpp:225-247).  Bar: identical ids,
+bit-identical scores, identical counts."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")]
+
+import paper_2605_02171_b200 as Q  # noqa: E402
+
+THREADS = os.cpu_count()
+
+
+def _same(r_ids, r_sc, r_cnt, ids, sc, cnt, what):
+    assert np.array_equal(np.asarray(r_cnt).view(np.uint32), cnt), what
+    assert np.array_equal(np.asarray(r_ids).view(np.uint32), ids), what
+    assert np.array_equal(np.asarray(r_sc).view(np.uint32), sc.view(np.uint32)), what
+
+
+# ------------------------------------------------------------- latency kernel
+_GRAPHS = {}
+
+
+def _ref_graph(dim):
+    """A reference-built graph at the BASELINE row width (R = 64, alpha 1.2)."""
+    if dim not in _GRAPHS:
+        from workloads.datasets import mixture
+        base, q = mixture(3_000, dim, 60, 0.3, seed=dim, nq=300, sigma_mode="norm")
+        ref = O.RefIndex.build(base, m=32, ef_c=64, alpha=1.2, threads=THREADS)
+        ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+        _GRAPHS[dim] = (ref, ix, q)
+    return _GRAPHS[dim]
+
+
+@pytest.mark.parametrize("dim", [768, 1536, 3072])
+@pytest.mark.parametrize("ef", [64, 256])
+def test_latency_kernel_vs_reference(dim, ef):
+    """Batch 1 and batch 128 (config 3's latency batches) through the public
+    call with host and with device-resident buffers: the launch must be the
+    latency kernel (stats warps_per_block == 4: one 4-warp CTA per query) and
+    every result identical to the reference's."""
+    import torch
+    ref, ix, q = _ref_graph(dim)
+    rid, rsc, rcnt = ref.run_query_batch(q, ef, 10, threads=THREADS)
+    for B in (1, 128):
+        for off in (0, 131) if B == 128 else (0, 17, 299):
+            qs = q[off:off + B]
+            # host buffers (qvg_search, the drop-in call)
+            ids, sc, cnt, st = ix.search(qs, k=10, ef=ef, stats=True)
+            assert st["warps_per_block"] == 4, (dim, ef, B, st["warps_per_block"])
+            sl = slice(off, off + B)
+            _same(rid[sl], rsc[sl], rcnt[sl], ids, sc, cnt, (dim, ef, B, off, "host"))
+            # device-resident queries and outputs
+            qd = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+            o_ids = torch.empty((B, 10), dtype=torch.int32, device="cuda")
+            o_sc = torch.empty((B, 10), dtype=torch.float32, device="cuda")
+            o_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
+            _, _, _, st = ix.search(qd, k=10, ef=ef, out=(o_ids, o_sc, o_cnt), stats=True)
+            assert st["warps_per_block"] == 4
+            _same(rid[sl], rsc[sl], rcnt[sl], o_ids.cpu().numpy().view(np.uint32),
+                  o_sc.cpu().numpy(), o_cnt.cpu().numpy().view(np.uint32),
+                  (dim, ef, B, off, "device"))
+
+
+def test_latency_kernel_single_query_api():
+    """qvg::query-style single calls (Q.query) — one query per launch."""
+    ref, ix, q = _ref_graph(768)
+    for i in (0, 5, 77):
+        r = Q.query(ix, q[i], Q.SearchParams(ef=64, k=10))
+        ids, sc = ref.query(q[i], 64, 10)
+        assert np.array_equal(r.ids, ids) and np.array_equal(r.scores.view(np.uint32),
+                                                             sc.view(np.uint32))
+
+
+# ------------------------------------------------------------------ tie stack
+def _tie_saturated(dim=8, n=2500, seed=5):
+    """Tiny D: SM2 distances take a handful of values, so pools fill with ties
+    and the reference expands long runs of evicted equal-distance nodes."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    base = rng.standard_normal((n, dim)).astype(np.float32)
+    q = rng.standard_normal((400, dim)).astype(np.float32)
+    ref = O.RefIndex.build(base, m=8, ef_c=32, alpha=1.2, threads=THREADS)
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    return ref, ix, q
+
+
+@pytest.mark.parametrize("ef", [16, 64])
+def test_tie_stack_overflow_is_rerun_not_an_error(ef):
+    """A query whose shared-memory tie stack fills is re-run with the stack in
+    global memory: the call never raises CapacityOverflow and every result,
+    pool and counter equals the reference / unbounded oracle."""
+    ref, ix, q = _tie_saturated()
+    rid, rsc, rcnt = ref.run_query_batch(q, ef, 10, threads=THREADS)
+    orc = O.OracleIndex.from_ref(ref)
+    # sorted-list restatement with an unbounded tie stack (its counters are
+    # the reference's expansion counts; pools equal the dual heap's)
+    o = orc.query_batch(q, ef, 10, mode=1, tie_cap=1 << 20, pools=True)
+    assert o["stats"]["tie_overflows"] == 0
+    saw_spill = False
+    for tcap in (0, 4, 8):  # default, then tiny shared-memory stacks
+        r = ix.search_ex(q, k=10, ef=ef, tie_capacity=tcap)
+        _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, (ef, tcap))
+        assert np.array_equal(r["pool_ids"], o["pool_ids"]), (ef, tcap)
+        assert np.array_equal(r["pool_dists"], o["pool_dists"]), (ef, tcap)
+        assert (r["status"] == 0).all()
+        assert r["stats"]["tie_expansions"] == o["stats"]["tie_expansions"], (ef, tcap)
+        saw_spill |= r["stats"]["tie_overflows"] > 0
+        if tcap == 4:
+            assert r["stats"]["tie_overflows"] > 0, "test graph does not exercise the spill"
+            assert r["stats"]["max_tie_depth"] > 4
+        # the drop-in call on the same batch (small -> latency kernel first)
+        ids, sc, cnt = ix.search(q[:100], k=10, ef=ef)
+        _same(ids, sc, cnt, rid[:100], rsc[:100], rcnt[:100], (ef, tcap, "search"))
+    assert saw_spill
+
+
+def test_tie_stack_spill_with_exact_visited_and_host_pipeline():
+    """The re-run also serves exact-visited launches and the pipelined host
+    upload (fused encode prologue: the re-run re-encodes the raw rows)."""
+    ref, ix, q0 = _tie_saturated(n=2500, seed=9)
+    q = np.concatenate([q0] * 6)  # 2400 rows: > 2 upload chunks -> pipelined path
+    rid, rsc, rcnt = ref.run_query_batch(q, 32, 10, threads=THREADS)
+    r = ix.search_ex(q, k=10, ef=32, tie_capacity=4, exact_visited=True)
+    _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, "exact")
+    assert r["stats"]["tie_overflows"] > 0
+    r = ix.search_ex(q, k=10, ef=32, tie_capacity=4)  # pipelined, fused prologue
+    _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, "pipelined")
+    assert r["stats"]["tie_overflows"] > 0
+    ids, sc, cnt = ix.search(q, k=10, ef=32)  # the public call, default capacity
+    _same(ids, sc, cnt, rid, rsc, rcnt, "public")
+
+
+# ------------------------------------------------- narrow rows, several rerank groups
+@pytest.mark.parametrize("dim", [8, 16, 48, 49, 96])
+def test_narrow_rows_rerank_more_than_32_rows(dim):
+    """D <= 48 makes the TMA rerank a single column slice per row group; with
+    ef > 32 the pool spans several 32-row groups (round-2 regression: the
+    round -> group division used a reciprocal that overflows for one slice).
+    Per-warp kernel (exact visited) and the default dispatch vs the reference."""
+    rng = np.random.Generator(np.random.PCG64(dim))
+    base = rng.standard_normal((2000, dim)).astype(np.float32)
+    q = rng.standard_normal((300, dim)).astype(np.float32)
+    ref = O.RefIndex.build(base, m=16, ef_c=64, alpha=1.2, threads=THREADS)
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    for ef in (33, 64, 100):
+        rid, rsc, rcnt = ref.run_query_batch(q, ef, 10, threads=THREADS)
+        for ex in (True, False):
+            r = ix.search_ex(q, k=10, ef=ef, exact_visited=ex)
+            _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, (dim, ef, ex))

@@ -143,7 +143,7 @@ def test_sorted_list_formulation_equals_reference_fresh_graph(sigma_mode):
     """SURVEY §8.A.3/4b on a fresh multi-threaded reference build: dual heap,
     sorted list with exact visited, and sorted list with tiny lossy visited tables
     all give the reference's ids, scores and pools."""
-    from paper_2605_02171_b200.datasets import mixture
+    from workloads.datasets import mixture
     base, q = mixture(6000, 128, 60, 0.35, seed=21, nq=150, sigma_mode=sigma_mode)
     ref = O.RefIndex.build(base, m=8, ef_c=32, alpha=1.2, threads=4)
     ix = O.OracleIndex.from_ref(ref)

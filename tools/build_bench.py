@@ -31,7 +31,7 @@ def main():
     import torch
 
     import paper_2605_02171_b200 as Q
-    from paper_2605_02171_b200 import datasets, graphs
+    from workloads import datasets, graphs
     cfg = datasets.CONFIGS[a.config]
     base, queries = datasets.config_data(cfg, n=a.n, nq=a.nq, sigma_mode=a.sigma_mode)
     n = base.shape[0]

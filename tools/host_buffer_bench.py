@@ -2,7 +2,7 @@ import sys, time, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 import paper_2605_02171_b200 as Q
-from paper_2605_02171_b200 import datasets, graphs
+from workloads import datasets, graphs
 cfg = datasets.CONFIGS[2]
 base, queries = datasets.config_data(cfg, nq=10000)
 g = graphs.load_graph(cfg, "literal", base.shape[0], base)

@@ -1,7 +1,7 @@
 import sys, time, numpy as np
 sys.path.insert(0, '/root/repo')
 import paper_2605_02171_b200 as Q
-from paper_2605_02171_b200 import datasets, graphs
+from workloads import datasets, graphs
 cfg = datasets.CONFIGS[2]
 base, queries = datasets.config_data(cfg, nq=1000)
 g = graphs.load_graph(cfg, "literal", base.shape[0], base)

@@ -11,7 +11,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2605_02171_b200 as Q  # noqa: E402
-from paper_2605_02171_b200 import datasets, graphs  # noqa: E402
+from workloads import datasets, graphs  # noqa: E402
 
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 import paper_2605_02171_b200 as Q  # noqa: E402
 from oracle.oracle import RefIndex  # noqa: E402
-from paper_2605_02171_b200 import datasets, graphs  # noqa: E402
+from workloads import datasets, graphs  # noqa: E402
 
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 mode = sys.argv[2] if len(sys.argv) > 2 else "literal"

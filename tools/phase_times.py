@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["QVG_VARIANT"] = str(16 | int(os.environ.get("EXTRA_VARIANT", "0")))
 import paper_2605_02171_b200 as Q
-from paper_2605_02171_b200 import datasets, graphs
+from workloads import datasets, graphs
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 vs = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 nq = int(sys.argv[3]) if len(sys.argv) > 3 else 10000

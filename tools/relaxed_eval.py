@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2605_02171_b200 as Q  # noqa: E402
-from paper_2605_02171_b200 import _native as N, datasets, graphs  # noqa: E402
+from paper_2605_02171_b200 import _native as N
+    from workloads import datasets, graphs  # noqa: E402
 
 cfgn = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 mode = sys.argv[2] if len(sys.argv) > 2 else "literal"

@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 import paper_2605_02171_b200 as Q
-from paper_2605_02171_b200 import _native as N, datasets, graphs
+from paper_2605_02171_b200 import _native as N
+    from workloads import datasets, graphs
 
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 base, queries = datasets.config_data(cfg, nq=10000)

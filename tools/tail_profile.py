@@ -16,7 +16,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2605_02171_b200 as Q  # noqa: E402
-from paper_2605_02171_b200 import datasets, graphs  # noqa: E402
+from workloads import datasets, graphs  # noqa: E402
 
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 ef = int(sys.argv[2]) if len(sys.argv) > 2 else 64

@@ -24,7 +24,8 @@ def child(a):
     import torch
 
     import paper_2605_02171_b200 as Q
-    from paper_2605_02171_b200 import _native as N, datasets, graphs
+    from paper_2605_02171_b200 import _native as N
+    from workloads import datasets, graphs
     cfg = datasets.CONFIGS[a.config]
     base, queries = datasets.config_data(cfg, nq=a.nq, sigma_mode=a.sigma_mode)
     g = graphs.load_graph(cfg, a.sigma_mode, base.shape[0], base)

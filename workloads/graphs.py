@@ -15,7 +15,7 @@ import numpy as np
 
 from .datasets import Config
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
 CACHE = os.environ.get("QVG_DATA_CACHE", os.path.join(ROOT, "data_cache"))
 
 
