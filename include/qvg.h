@@ -227,6 +227,22 @@ typedef struct qvg_build_stats {
 qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim, const qvg_build_params* p,
                      int device, qvg_index** out, qvg_build_stats* stats);
 
+/* qivr::robust_prune (graph.hpp:162-183), batched, with dist_fn = the SM2
+ * distance of the index's codes (SignatureStore::distance, as link_node /
+ * insert_bidirectional bind it, builder.cpp:130-131).  Task t prunes the
+ * candidates cand_ids/cand_dists[offsets[t], offsets[t+1]) (cand_dists =
+ * dist(c, target), the Candidate::dist the caller computed): ascending (dist,
+ * id), c kept iff float(c.dist) <= alpha * float(dist(c, s)) for every kept s,
+ * at most max_degree kept.  Output: out_ids[t * max_degree ...] (unused slots
+ * UINT32_MAX), out_count[t].  The builder's own prune kernel (qvg_build) runs
+ * it.  Candidate ids must be distinct within a task (they are at every
+ * reference call site); at most 256 per task; 1 <= max_degree <= 128.  All
+ * pointers host or device. */
+qvg_status qvg_robust_prune(qvg_index* index, uint64_t ntasks, const uint64_t* offsets,
+                            const uint32_t* cand_ids, const uint32_t* cand_dists,
+                            uint32_t max_degree, float alpha, uint32_t* out_ids,
+                            uint32_t* out_count);
+
 /* ---- evaluation support ------------------------ */
 
 /* Scorers of qivr::Scorer (eval.hpp:13). */

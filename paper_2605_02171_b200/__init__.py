@@ -312,6 +312,28 @@ class GpuIndex:
                                        pi.ctypes.data, pd.ctypes.data, pn.ctypes.data, None))
         return pi, pd, pn
 
+    def robust_prune(self, candidates, max_degree, alpha):
+        """qivr::robust_prune (graph.hpp:162-183) on the GPU for a batch of
+        candidate lists: `candidates` is a list of (ids, dists) pairs (dists =
+        the candidates' BQ distances to their target) -> list of kept-id arrays.
+        dist_fn(a, b) is the SM2 distance of the index's codes."""
+        ids = [np.ascontiguousarray(c[0], np.uint32).reshape(-1) for c in candidates]
+        dst = [np.ascontiguousarray(c[1], np.uint32).reshape(-1) for c in candidates]
+        if any(a.size != b.size for a, b in zip(ids, dst)):
+            raise InvalidArgument("robust_prune: ids and dists differ in length")
+        off = np.zeros(len(ids) + 1, np.uint64)
+        off[1:] = np.cumsum([a.size for a in ids])
+        all_ids = np.concatenate(ids) if ids else np.empty(0, np.uint32)
+        all_d = np.concatenate(dst) if dst else np.empty(0, np.uint32)
+        out = np.empty((max(len(ids), 1), max_degree), np.uint32)
+        cnt = np.empty(max(len(ids), 1), np.uint32)
+        _check(N.lib().qvg_robust_prune(self._h, len(ids), off.ctypes.data,
+                                        all_ids.ctypes.data if all_ids.size else None,
+                                        all_d.ctypes.data if all_d.size else None,
+                                        max_degree, float(alpha), out.ctypes.data,
+                                        cnt.ctypes.data))
+        return [out[t, : cnt[t]].copy() for t in range(len(ids))]
+
     def sm2_distance(self, query_codes, ids):
         qc = np.ascontiguousarray(query_codes, np.uint64).reshape(-1, 2 * self.W)
         ids = np.ascontiguousarray(ids, np.uint32).reshape(-1)

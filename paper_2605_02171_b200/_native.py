@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "qvg_index_save", "qvg_index_destroy", "qvg_index_info", "qvg_index_set_stream",
     "qvg_index_export", "qvg_search", "qvg_search_ex", "qvg_beam_search", "qvg_encode",
     "qvg_sm2_distance", "qvg_build", "qvg_brute_force_topk", "qvg_compatibility_probe",
-    "qvg_strong_bit_rate", "qvg_encode_rows",
+    "qvg_strong_bit_rate", "qvg_encode_rows", "qvg_robust_prune",
 )
 
 
@@ -112,6 +112,7 @@ def lib():
     L.qvg_compatibility_probe.argtypes = [i32, vp, u64, u32, u64, u32, i32,
                                           C.POINTER(qvg_probe_report)]
     L.qvg_encode_rows.argtypes = [i32, vp, u64, u32, i32, vp, vp]
+    L.qvg_robust_prune.argtypes = [vp, u64, vp, vp, vp, u32, C.c_float, vp, vp]
     L.qvg_strong_bit_rate.argtypes = [vp, vp, u64, u32, i32, C.POINTER(qvg_encoding_diagnostics)]
     for name in EXPORTED_SYMBOLS:
         f = getattr(L, name)

@@ -45,7 +45,11 @@ namespace {
 
 using namespace dev;
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr uint32_t kMaxCand = 256;  // candidates per prune task (closest kept)
+// candidates a prune task holds: the kMaxCand closest by (dist, id) of its
+// existing row and new candidates (streamed in chunks of 32; kCandBuf is the
+// bitonic-sort capacity of kMaxCand + 32 rounded to a power of two)
+constexpr uint32_t kMaxCand = 256;
+constexpr uint32_t kCandBuf = 512;
 
 // ---- stage 0: entry point (builder.cpp:90-120) --------------------------------
 __global__ void centroid_kernel(const float* __restrict__ cold, uint64_t n, uint32_t dim,
@@ -154,6 +158,11 @@ struct PruneArgs {
     uint32_t R;
     unsigned long long* reprunes;
     unsigned long long* counter;   // task queue
+    // function-level mode (qvg_robust_prune): task t's selection goes to
+    // out_sel[t*R ...) and its size to out_cnt[t] instead of the adjacency row;
+    // targets may be null (no target: every distance is given)
+    uint32_t* out_sel;
+    uint32_t* out_cnt;
 };
 
 constexpr int kPruneWarps = 2;
@@ -173,7 +182,7 @@ __host__ __device__ inline PruneSmem prune_layout(uint32_t W, uint32_t R) {
     };
     const uint32_t gs = (64u * W + 127u) & ~127u;  // 4-row TMA group
     L.bar = take(16, 16);
-    L.keys_off = take(8 * kMaxCand, 16);
+    L.keys_off = take(8 * kCandBuf, 16);
     L.sel_ids = take(4 * R, 16);
     L.sel_codes = take(16 * W * R, 16);
     L.stage = take(8 * gs, 128);  // 32 candidate rows per TMA round
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
         tt = __shfl_sync(kFull, tt, 0);
         if (tt >= a.ntasks) break;
         const uint32_t t = (uint32_t)tt;
-        const uint32_t v = a.targets[t];
+        const uint32_t v = a.targets ? a.targets[t] : kSentinel;
         uint32_t lo, hi;
         if (a.seg) {
             lo = a.seg[t];
@@ -243,8 +252,9 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
             lo = t * a.stride;
             hi = lo + a.counts[t];
         }
-        uint32_t* vrow = a.adj + (size_t)v * ix.RS;
-        for (uint32_t w = lane; w < W; w += 32) vc[w] = ix.codes[(size_t)v * W + w];
+        uint32_t* vrow = v != kSentinel ? a.adj + (size_t)v * ix.RS : nullptr;
+        if (v != kSentinel)
+            for (uint32_t w = lane; w < W; w += 32) vc[w] = ix.codes[(size_t)v * W + w];
         // existing row (kept in registers: slot lane*... up to R <= 128)
         uint32_t ex[4];
         uint32_t nex = 0;
@@ -293,63 +303,79 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
             }
             if (lane == 0) atomicAdd(a.reprunes, 1ull);
         }
-        // ---- candidate keys (dist<<32 | id): new candidates + existing row
-        uint32_t nc = 0;
-        const uint32_t nnew_c = min(nnew, kMaxCand - min(nex, kMaxCand));
-        for (uint32_t i0 = 0; i0 < nnew_c; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            if (i < nnew_c) {
-                const uint32_t c = a.cand_ids[lo + i];
-                const uint32_t d = a.cand_dists ? a.cand_dists[lo + i] : kSentinel;
-                keys[i] = ((uint64_t)d << 32) | c;
+        // d(v, c) for the keys in [b, e) whose distance is unknown (TMA-staged
+        // rows, lane per row)
+        auto score_unknown = [&](uint32_t b, uint32_t e) {
+            for (uint32_t r0 = b; r0 < e; r0 += 32) {
+                const uint32_t cnt = min(32u, e - r0);
+                bool unknown = false;
+                if (lane < cnt) unknown = (keys[r0 + lane] >> 32) == kSentinel;
+                if (!__any_sync(kFull, unknown)) continue;
+                fetch(nullptr, keys, r0, cnt);
+                if (unknown) {
+                    const uint4* rp = srow(lane);
+                    uint32_t d = 0;
+                    for (uint32_t w = 0; w < W; ++w) d += sm2_chunk(vc[w], rp[w]);
+                    keys[r0 + lane] = ((uint64_t)d << 32) | (uint32_t)keys[r0 + lane];
+                }
+                __syncwarp();
             }
-        }
-        nc = nnew_c;
+        };
+        // ascending (dist, id) order of keys[0, cnt) (bitonic over the next power of two)
+        auto sort_keys = [&](uint32_t cnt) {
+            uint32_t np2 = 1;
+            while (np2 < cnt) np2 <<= 1;
+            for (uint32_t i = cnt + lane; i < np2; i += 32) keys[i] = ~0ull;
+            __syncwarp();
+            for (uint32_t size = 2; size <= np2; size <<= 1) {
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t i = lane; i < np2; i += 32) {
+                        const uint32_t j = i ^ stride;
+                        if (j > i) {
+                            const uint64_t x = keys[i], y = keys[j];
+                            const bool up = (i & size) == 0;
+                            if ((x > y) == up) {
+                                keys[i] = y;
+                                keys[j] = x;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        };
+        // ---- candidate keys (dist<<32 | id): the existing row, then the new
+        // candidates in chunks of 32.  Whenever more than kMaxCand are held the
+        // unknown distances are computed and only the kMaxCand closest keys by
+        // (dist, id) are kept, so a hub target that receives thousands of
+        // reverse edges in one batch still re-prunes over its closest
+        // candidates (graph.hpp:207-226 re-prunes over row + node)
+        uint32_t nc = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const bool have = ex[j] != kSentinel;
             const unsigned b = __ballot_sync(kFull, have);
-            if (have && nc + __popc(b & lt_mask) < kMaxCand)
-                keys[nc + __popc(b & lt_mask)] = ((uint64_t)kSentinel << 32) | ex[j];
-            nc = min(kMaxCand, nc + __popc(b));
+            if (have) keys[nc + __popc(b & lt_mask)] = ((uint64_t)kSentinel << 32) | ex[j];
+            nc += __popc(b);
         }
-        __syncwarp();
-        // ---- distances d(v, c) where unknown (TMA-staged rows, lane per row)
-        for (uint32_t r0 = 0; r0 < nc; r0 += 32) {
-            const uint32_t cnt = min(32u, nc - r0);
-            bool any_unknown = false;
-            if (lane < cnt) any_unknown = (keys[r0 + lane] >> 32) == kSentinel;
-            if (!__any_sync(kFull, any_unknown)) continue;
-            fetch(nullptr, keys, r0, cnt);
-            if (lane < cnt && any_unknown) {
-                const uint4* rp = srow(lane);
-                uint32_t d = 0;
-                for (uint32_t w = 0; w < W; ++w) d += sm2_chunk(vc[w], rp[w]);
-                keys[r0 + lane] = ((uint64_t)d << 32) | (uint32_t)keys[r0 + lane];
+        for (uint32_t i0 = 0; i0 < nnew; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            if (i < nnew) {
+                const uint32_t c = a.cand_ids[lo + i];
+                const uint32_t d = a.cand_dists ? a.cand_dists[lo + i] : kSentinel;
+                keys[nc + lane] = ((uint64_t)d << 32) | c;
             }
+            nc += min(32u, nnew - i0);
             __syncwarp();
-        }
-        // ---- sort keys ascending (bitonic over the next power of two)
-        uint32_t np2 = 1;
-        while (np2 < nc) np2 <<= 1;
-        for (uint32_t i = nc + lane; i < np2; i += 32) keys[i] = ~0ull;
-        __syncwarp();
-        for (uint32_t size = 2; size <= np2; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = lane; i < np2; i += 32) {
-                    const uint32_t j = i ^ stride;
-                    if (j > i) {
-                        const uint64_t x = keys[i], y = keys[j];
-                        const bool up = (i & size) == 0;
-                        if ((x > y) == up) {
-                            keys[i] = y;
-                            keys[j] = x;
-                        }
-                    }
-                }
-                __syncwarp();
+            if (nc > kMaxCand) {
+                score_unknown(0, nc);
+                sort_keys(nc);
+                nc = kMaxCand;
             }
         }
+        __syncwarp();
+        score_unknown(0, nc);
+        sort_keys(nc);
         // ---- greedy RobustPrune (graph.hpp:162-183)
         uint32_t ns = 0;
         for (uint32_t r0 = 0; r0 < nc && ns < a.R; r0 += 32) {
@@ -377,7 +403,12 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
             }
         }
         __syncwarp();
-        for (uint32_t s = lane; s < ix.RS; s += 32) vrow[s] = s < ns ? sel[s] : kSentinel;
+        if (a.out_sel) {
+            for (uint32_t s = lane; s < ns; s += 32) a.out_sel[(size_t)t * a.R + s] = sel[s];
+            if (lane == 0) a.out_cnt[t] = ns;
+        } else {
+            for (uint32_t s = lane; s < ix.RS; s += 32) vrow[s] = s < ns ? sel[s] : kSentinel;
+        }
         __syncwarp();
     }
 }
@@ -653,4 +684,128 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
     }
     *out = h;
     return QVG_OK;
+}
+
+// qivr::robust_prune (graph.hpp:162-183) as a batched device call over the
+// index's BQ codes: the builder's own prune kernel in function-level mode.
+extern "C" qvg_status qvg_robust_prune(qvg_index* h, uint64_t ntasks, const uint64_t* offsets,
+                                       const uint32_t* cand_ids, const uint32_t* cand_dists,
+                                       uint32_t max_degree, float alpha, uint32_t* out_ids,
+                                       uint32_t* out_count) {
+    if (!h || !offsets || !out_count || (ntasks && !out_ids)) {
+        set_error("qvg_robust_prune: null argument");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (max_degree < 1 || max_degree > kMaxDegree) {
+        set_error("qvg_robust_prune: max_degree must be in [1, 128]");
+        return QVG_INVALID_ARGUMENT;
+    }
+    if (ntasks == 0) return QVG_OK;
+    if (!h->has_tmap) {
+        set_error("qvg_robust_prune: code rows too wide for the TMA gather (W > 128)");
+        return QVG_NOT_IMPLEMENTED;
+    }
+    std::lock_guard<std::mutex> lock(h->mu);
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    const DevIndex& ix = h->ix;
+    std::vector<uint64_t> off(ntasks + 1);
+    e = cudaMemcpy(off.data(), offsets, (ntasks + 1) * 8, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_status(e, "qvg_robust_prune: offsets");
+    if (off[0] != 0) {
+        set_error("qvg_robust_prune: offsets[0] must be 0");
+        return QVG_INVALID_ARGUMENT;
+    }
+    for (uint64_t t = 0; t < ntasks; ++t) {
+        if (off[t + 1] < off[t]) {
+            set_error("qvg_robust_prune: offsets must be non-decreasing");
+            return QVG_INVALID_ARGUMENT;
+        }
+        if (off[t + 1] - off[t] > kMaxCand) {
+            set_error("qvg_robust_prune: more than 256 candidates in one task");
+            return QVG_NOT_IMPLEMENTED;
+        }
+    }
+    const uint64_t total = off[ntasks];
+    if (total >= 0xFFFFFFFFull) {
+        set_error("qvg_robust_prune: too many candidates");
+        return QVG_NOT_IMPLEMENTED;
+    }
+    if (total && (!cand_ids || !cand_dists)) {
+        set_error("qvg_robust_prune: null candidates");
+        return QVG_INVALID_ARGUMENT;
+    }
+    std::vector<uint32_t> ids(total), seg(ntasks + 1);
+    if (total) {
+        e = cudaMemcpy(ids.data(), cand_ids, total * 4, cudaMemcpyDefault);
+        if (e != cudaSuccess) return cuda_status(e, "qvg_robust_prune: candidates");
+    }
+    for (uint64_t i = 0; i < total; ++i)
+        if (ids[i] >= ix.n) {
+            set_error("qvg_robust_prune: candidate id out of range");
+            return QVG_INVALID_ARGUMENT;
+        }
+    for (uint64_t t = 0; t <= ntasks; ++t) seg[t] = (uint32_t)off[t];
+    cudaStream_t s = h->stream;
+    std::vector<void*> tmp;
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaMalloc(&q, bytes < 16 ? 16 : bytes) != cudaSuccess) return nullptr;
+        tmp.push_back(q);
+        return q;
+    };
+    auto done = [&](qvg_status st) {
+        cudaStreamSynchronize(s);
+        for (void* q : tmp) cudaFree(q);
+        return st;
+    };
+    uint32_t* d_ids = static_cast<uint32_t*>(dalloc(total * 4));
+    uint32_t* d_dst = static_cast<uint32_t*>(dalloc(total * 4));
+    uint32_t* d_seg = static_cast<uint32_t*>(dalloc((ntasks + 1) * 4));
+    uint32_t* d_sel = static_cast<uint32_t*>(dalloc(ntasks * max_degree * 4));
+    uint32_t* d_cnt = static_cast<uint32_t*>(dalloc(ntasks * 4));
+    unsigned long long* d_ctr = static_cast<unsigned long long*>(dalloc(16));
+    if (!d_ids || !d_dst || !d_seg || !d_sel || !d_cnt || !d_ctr)
+        return done(cuda_status(cudaErrorMemoryAllocation, "qvg_robust_prune"));
+    e = cudaMemcpyAsync(d_ids, ids.data(), total * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_dst, cand_dists, total * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_seg, seg.data(), (ntasks + 1) * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_ctr, 0, 16, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_sel, 0xFF, ntasks * max_degree * 4, s);
+    if (e != cudaSuccess) return done(cuda_status(e, "qvg_robust_prune: upload"));
+    PruneArgs pa{};
+    pa.ix = ix;
+    pa.adj = const_cast<uint32_t*>(ix.adj);  // not written in function-level mode
+    pa.ntasks = (uint32_t)ntasks;
+    pa.targets = nullptr;
+    pa.cand_ids = d_ids;
+    pa.cand_dists = d_dst;
+    pa.seg = d_seg;
+    pa.alpha = alpha;
+    pa.R = max_degree;
+    pa.reprunes = d_ctr + 1;
+    pa.counter = d_ctr;
+    pa.out_sel = d_sel;
+    pa.out_cnt = d_cnt;
+    const PruneSmem PL = prune_layout(ix.W, max_degree);
+    const uint32_t pwb = PL.total, pblock = pwb * kPruneWarps;
+    e = cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pblock);
+    if (e != cudaSuccess) return done(cuda_status(e, "qvg_robust_prune: smem"));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prune_kernel, kPruneWarps * 32, pblock);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    if (per_sm < 1) {
+        set_error("qvg_robust_prune: prune kernel does not fit (code rows too wide)");
+        return done(QVG_NOT_IMPLEMENTED);
+    }
+    uint64_t g = (ntasks + kPruneWarps - 1) / kPruneWarps;
+    if (g > (uint64_t)per_sm * sms) g = (uint64_t)per_sm * sms;
+    prune_kernel<<<(unsigned)g, kPruneWarps * 32, pblock, s>>>(h->tmap, pa, pwb);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out_ids, d_sel, ntasks * max_degree * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_count, d_cnt, ntasks * 4, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return done(e == cudaSuccess ? QVG_OK : cuda_status(e, "qvg_robust_prune"));
 }

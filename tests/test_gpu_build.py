@@ -38,7 +38,7 @@ def build(data, m, ef_c, alpha=1.2, passes=1, batch=0, seed=42):
 @ref_only
 @pytest.mark.parametrize("passes", [1, 2])
 def test_build_stage0_exact_and_graph_quality(passes):
-    base, q = mixture(6000, 96, 40, 0.35, seed=5, nq=200, sigma_mode="norm")
+    base, q = mixture(6000, 96, 40, 0.35, seed=5, nq=1000, sigma_mode="norm")
     ix, st = build(base, m=8, ef_c=48, passes=passes, batch=512)
     codes, adj, cold = ix.export()
     ref = O.RefIndex.build(base, m=8, ef_c=48, alpha=1.2, threads=4)
@@ -61,7 +61,8 @@ def test_build_stage0_exact_and_graph_quality(passes):
     rids, _, _ = ref.run_query_batch(q, 64, 10, threads=4)
     rec = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids, gt)])
     rrec = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(rids, gt)])
-    assert rec >= rrec - 0.05, (rec, rrec)
+    # BASELINE config 5 bar: within 0.5 points of the reference-built graph
+    assert rec >= rrec - (0.005 if passes == 2 else 0.02), (rec, rrec)
 
 
 def test_build_is_deterministic_and_searchable():
@@ -98,3 +99,51 @@ def test_gpu_graph_searches_identically_on_the_reference():
         ids, sc, _ = ix.search(q, 10, ef)
         assert np.array_equal(ids, rids)
         assert np.array_equal(sc.view(np.uint32), rsc.view(np.uint32))
+
+
+@ref_only
+@pytest.mark.parametrize("R", [16, 32, 64])
+def test_gpu_robust_prune_equals_reference_function(R):
+    """Function-level parity of the builder's prune kernel (qvg_robust_prune)
+    with qivr::robust_prune (graph.hpp:162-183) on identical candidate lists:
+    heavy distance ties (tiny-D codes: pairwise SM2 distances take a handful of
+    values; candidate dists drawn from a small range or equal to the true
+    distance to a target), alpha in {1.0, 1.2}, up to 256 candidates."""
+    rng = np.random.Generator(np.random.PCG64(R))
+    for dim, n in ((8, 3000), (64, 3000), (768, 1500)):
+        base = rng.standard_normal((n, dim)).astype(np.float32)
+        ref = O.RefIndex.build(base, m=4, ef_c=16, alpha=1.2, threads=8)
+        ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+        codes = ref.codes()
+        tasks = []
+        for t in range(120):
+            nc = int(rng.integers(1, 257))
+            ids = rng.choice(n, nc, replace=False).astype(np.uint32)
+            if t % 3 == 0:  # dists = true BQ distance to a target (as link_node)
+                tgt = int(rng.integers(0, n))
+                ids = ids[ids != tgt]
+                d = np.array([O.ref_sm2(codes[tgt], codes[i]) for i in ids], np.uint32)
+            elif t % 3 == 1:  # a tiny range: massive (dist, id) ordering by id
+                d = rng.integers(0, 4, ids.size).astype(np.uint32)
+            else:
+                d = rng.integers(0, 3 * dim // 2 + 2, ids.size).astype(np.uint32)
+            tasks.append((ids, d))
+        for alpha in (1.0, 1.2):
+            got = ix.robust_prune(tasks, R, alpha)
+            for t, (ids, d) in enumerate(tasks):
+                want = ref.robust_prune(ids, d, R, alpha)
+                assert np.array_equal(got[t], want), (dim, alpha, t)
+
+
+@ref_only
+def test_gpu_robust_prune_validates_like_a_boundary():
+    base = np.random.Generator(np.random.PCG64(1)).standard_normal((100, 16)).astype(np.float32)
+    ref = O.RefIndex.build(base, m=4, ef_c=16, alpha=1.2, threads=4)
+    ix = Q.GpuIndex.from_arrays(ref.codes(), ref.adjacency(), ref.cold(), ref.entry)
+    with pytest.raises(Q.InvalidArgument):
+        ix.robust_prune([(np.array([100], np.uint32), np.array([1], np.uint32))], 8, 1.2)
+    with pytest.raises(Q.NotImplementedByQvg):
+        ix.robust_prune([(np.arange(100, dtype=np.uint32).repeat(3)[:257],
+                          np.zeros(257, np.uint32))], 8, 1.2)
+    assert [a.tolist() for a in ix.robust_prune([(np.empty(0, np.uint32),
+                                                  np.empty(0, np.uint32))], 8, 1.2)] == [[]]
