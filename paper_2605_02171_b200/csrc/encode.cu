@@ -9,11 +9,13 @@
 //                          strict, pad bits zero)
 // The double reductions must run in index order to round identically, so one
 // lane owns one query's chain and the batch supplies the parallelism.
-// Kernels (QVG_ENCODE selects; all bit-exact, tests/test_gpu_parity.py):
-//   0 encode_lpq_kernel   (default) lane per query, rows staged in shared memory
-//   1 encode_tiled_kernel lane per query through 32x32 transposed tiles
-//   2 encode_warp_kernel  warp per query, lane 0 runs the chains
-//   3 encode_block_kernel lane per query, TMA-staged block of rows
+// Kernels (all bit-exact, tests/test_gpu_parity.py):
+//   encode_lpq_kernel   (default) lane per query, rows staged in shared memory
+//   encode_tiled_kernel lane per query through 32x32 transposed tiles (rows too
+//                       wide for the staging buffer)
+//   encode_warp_kernel  warp per query, lane 0 runs the chains
+// QVG_ENCODE=1 / 2 forces the tiled / warp kernel (test hook, not a tuning
+// surface: the default is the measured-fastest for every BASELINE geometry).
 // All arithmetic uses explicit _rn intrinsics so no contraction can change a
 // rounding.
 #include <algorithm>
@@ -345,116 +347,6 @@ __global__ void __launch_bounds__(256) encode_warp_kernel(
     }
 }
 
-// Block-of-rows variant: one warp owns QB consecutive queries (their rows are
-// contiguous in x), staged on chip by a single TMA bulk copy; lane l runs query
-// l's reductions in index order.  Rows sit unpadded (row stride D floats), so
-// the traversal is time-skewed: at step t lane l reads column t - l, which puts
-// the 32 lanes on 32 different banks at every step (for D a multiple of 32).
-__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
-}
-
-__global__ void __launch_bounds__(32) encode_block_kernel(
-    const float* __restrict__ x, uint64_t nq, uint32_t dim, uint32_t Dp, uint32_t QB,
-    float* __restrict__ qn, uint4* __restrict__ qcodes, float* __restrict__ tau_out,
-    int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
-    extern __shared__ __align__(128) float blk[];  // QB x dim floats, then the mbarrier
-    const uint32_t lane = threadIdx.x;
-    const uint64_t q0 = (uint64_t)blockIdx.x * QB;
-    const uint32_t rows = (nq - q0) < QB ? (uint32_t)(nq - q0) : QB;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(blk + (((size_t)QB * dim + 3) & ~(size_t)3));
-    const uint32_t bytes = rows * dim * 4u;
-    if (lane == 0) {
-        mbar_init1(bar);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(bar)),
-                     "r"(bytes)
-                     : "memory");
-        // bulk copies of <= 64 KB (16-B multiples: dim % 4 == 0 is required)
-        for (uint32_t off = 0; off < bytes; off += 65536u) {
-            const uint32_t len = min(65536u, bytes - off);
-            asm volatile(
-                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    (uint32_t)__cvta_generic_to_shared(reinterpret_cast<char*>(blk) + off)),
-                "l"(reinterpret_cast<const char*>(x + q0 * dim) + off), "r"(len),
-                "r"((uint32_t)__cvta_generic_to_shared(bar))
-                : "memory");
-        }
-    }
-    __syncwarp();
-    asm volatile(
-        "{\n .reg .pred p;\n QVG_EWAIT:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-        " @!p bra QVG_EWAIT;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar))
-        : "memory");
-    const bool mine = lane < rows;
-    float* row = blk + (size_t)(mine ? lane : 0) * dim;
-    const uint32_t steps = dim + 31;
-    // pass 1: finite + sequential sum of squares
-    bool finite = true;
-    double acc = 0.0;
-    for (uint32_t t = 0; t < steps; ++t) {
-        const uint32_t j = t - lane;
-        if (mine && t >= lane && j < dim) {
-            const float v = row[j];
-            finite &= finitef(v);
-            acc = __fma_rn((double)v, (double)v, acc);
-        }
-    }
-    int32_t st = QVG_Q_OK;
-    if (!finite) st = QVG_Q_NONFINITE_COORD;
-    const double norm = __dsqrt_rn(acc);
-    if (st == QVG_Q_OK && (!(norm > 0.0) || isinf(norm))) st = QVG_Q_BAD_NORM;
-    const float inv = st == QVG_Q_OK ? __double2float_rn(__ddiv_rn(1.0, norm)) : 0.0f;
-    // pass 2: y = x * inv in place, finite check, sequential sum of |y|
-    double s = 0.0;
-    bool yfinite = true;
-    for (uint32_t t = 0; t < steps; ++t) {
-        const uint32_t j = t - lane;
-        if (mine && t >= lane && j < dim) {
-            const float y = st == QVG_Q_OK ? __fmul_rn(row[j], inv) : 0.0f;
-            yfinite &= finitef(y);
-            s = __dadd_rn(s, fabs((double)y));
-            row[j] = y;
-        }
-    }
-    if (st == QVG_Q_OK && !yfinite) st = QVG_Q_NONFINITE_CODE;
-    const float tau = st == QVG_Q_OK ? __double2float_rn(__ddiv_rn(s, (double)dim)) : 0.0f;
-    // pass 3: bit planes, skewed; a word is emitted when its last column passes
-    const uint32_t W = (dim + 63) / 64;
-    uint32_t p0 = 0, p1 = 0, s0 = 0, s1 = 0;
-    for (uint32_t t = 0; t < steps; ++t) {
-        const uint32_t j = t - lane;
-        if (mine && t >= lane && j < dim) {
-            const float y = row[j];
-            const uint32_t b = j & 63u;
-            const uint32_t pb = y > 0.0f, sb = fabsf(y) > tau;
-            if (b < 32) {
-                p0 |= pb << b;
-                s0 |= sb << b;
-            } else {
-                p1 |= pb << (b - 32);
-                s1 |= sb << (b - 32);
-            }
-            if (b == 63 || j == dim - 1) {
-                qcodes[(q0 + lane) * W + j / 64] =
-                    st == QVG_Q_OK ? make_uint4(p0, p1, s0, s1) : make_uint4(0, 0, 0, 0);
-                p0 = p1 = s0 = s1 = 0;
-            }
-        }
-    }
-    __syncwarp();
-    // normalised rows out, coalesced (zero pad to Dp)
-    for (uint32_t r = 0; r < rows; ++r)
-        for (uint32_t c = lane; c < Dp; c += 32) qn[(q0 + r) * Dp + c] = c < dim ? blk[(size_t)r * dim + c] : 0.0f;
-    if (mine) {
-        status[q0 + lane] = st;
-        if (st != QVG_Q_OK && flags) atomicOr(flags, 1u << st);
-        if (tau_out) tau_out[q0 + lane] = tau;
-    }
-}
-
 // reference layout (W pos words, W strong words per row) -> 16-B chunks
 __global__ void codes_to_chunks_kernel(const uint64_t* __restrict__ ref, uint64_t rows,
                                        uint32_t W, uint4* __restrict__ out) {
@@ -489,18 +381,6 @@ void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float
         const char* v = getenv("QVG_ENCODE");
         return v ? atoi(v) : 0;
     }();
-    const bool aligned = (dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    uint32_t QB = (uint32_t)((200u * 1024u - 16u) / (dim * 4u));
-    if (QB > 32) QB = 32;
-    if (variant == 3 && aligned && QB >= 8) {  // opt-in: measured slower (0.27 vs 0.15 ms)
-        const size_t bsmem = (((size_t)QB * dim + 3) & ~(size_t)3) * 4 + 16;
-        cudaFuncSetAttribute(encode_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)bsmem);
-        const unsigned blocks = (unsigned)((nq + QB - 1) / QB);
-        encode_block_kernel<<<blocks, 32, bsmem, s>>>(x, nq, dim, Dp, QB, qn, qcodes, tau, status,
-                                                       flags);
-        return;
-    }
     if (variant == 0) {
         // largest QB (<= 32 queries per block) that still fits the batch in one
         // wave of resident blocks; QB = 32 when no QB does (large batches)

@@ -370,10 +370,17 @@ qvg_status qvg_index_load(const char* path, int device, qvg_index** out) {
         st = QVG_RUNTIME_ERROR;
         set_error("load_index: cold segment read failed");
     }
+    // one event per staging buffer: reading chunk i+1 from the file overlaps the
+    // H2D copy of chunk i (waiting on the stream would also wait for the other
+    // buffer's copy and serialise file read and upload)
+    cudaEvent_t freed[2] = {nullptr, nullptr};
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[1], cudaEventDisableTiming);
+    bool used[2] = {false, false};
     int buf = 0;
     for (uint64_t r0 = 0; e == cudaSuccess && st == QVG_OK && r0 < H.n; r0 += chunk_rows) {
         const uint64_t rows = std::min<uint64_t>(chunk_rows, H.n - r0);
-        e = cudaStreamSynchronize(h->stream);  // staging buffer `buf` is free again
+        if (used[buf]) e = cudaEventSynchronize(freed[buf]);  // this buffer's last copy is done
         if (e != cudaSuccess) break;
         if (fread(pinned[buf], 4ull * H.dim, rows, f.get()) != rows) {
             st = QVG_RUNTIME_ERROR;
@@ -387,9 +394,14 @@ qvg_status qvg_index_load(const char* path, int device, qvg_index** out) {
         else
             e = cudaMemcpy2DAsync(dst, h->ix.Dp * 4, pinned[buf], H.dim * 4, H.dim * 4, rows,
                                   cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(freed[buf], h->stream);
+        used[buf] = true;
         buf ^= 1;
     }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    const cudaError_t es = cudaStreamSynchronize(h->stream);  // never free a buffer in use
+    if (e == cudaSuccess) e = es;
+    for (cudaEvent_t ev : freed)
+        if (ev) cudaEventDestroy(ev);
     cudaFreeHost(pinned[0]);
     cudaFreeHost(pinned[1]);
     if (e != cudaSuccess) st = cuda_status(e, "load_index: cold upload");

@@ -141,7 +141,6 @@ print("OK")
 
 
 @pytest.mark.parametrize("env", [{"QVG_FUSED": "1"}, {"QVG_ENCODE": "1"}, {"QVG_ENCODE": "2"},
-                                 {"QVG_ENCODE": "3"},
                                  {"QVG_VARIANT": "8"},
                                  {"QVG_VARIANT": "13"}, {"QVG_STAGE_HALF_BYTES": "512"},
                                  {"QVG_SPLIT_MAX_ROWS": "32"},

@@ -4,6 +4,7 @@
 
 `dev`: queries already in HBM (the bench's `value` path: separate encode
 kernel); default: host queries (pipelined upload + fused encode prologue).
+A 6th argument picks the generator's sigma mode (literal | norm).
 """
 import os
 import sys
@@ -16,10 +17,11 @@ from workloads import datasets, graphs  # noqa: E402
 cfg = datasets.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
 ef = int(sys.argv[3]) if len(sys.argv) > 3 else 64
-base, queries = datasets.config_data(cfg, nq=nq)
-g = graphs.load_graph(cfg, "literal", base.shape[0], base)
+mode = sys.argv[5] if len(sys.argv) > 5 else "literal"
+base, queries = datasets.config_data(cfg, nq=nq, sigma_mode=mode)
+g = graphs.load_graph(cfg, mode, base.shape[0], base)
 if g is None:
-    g = graphs.load_graph(cfg, "literal", base.shape[0], base, builder="gpu")
+    g = graphs.load_graph(cfg, mode, base.shape[0], base, builder="gpu")
 if g is None:
     bi = Q.GpuIndex.build(base, Q.BuildParams(m=cfg.m, ef_c=cfg.ef_c, alpha=cfg.alpha))
     _, adj, _ = bi.export()
