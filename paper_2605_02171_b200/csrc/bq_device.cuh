@@ -60,6 +60,14 @@ __device__ __forceinline__ void bulk_row(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// warm L2 with a small range through the LSU (one prefetch per 128-B line):
+// unlike the bulk prefetch it does not queue behind the TMA gathers
+__device__ __forceinline__ void prefetch_lines_l2(const void* src, uint32_t bytes) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(127);
+    const uintptr_t a1 = reinterpret_cast<uintptr_t>(src) + bytes;
+    for (uintptr_t a = a0; a < a1; a += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 // order this thread's generic-proxy smem accesses before later async-proxy
 // (TMA) writes to the same smem
 __device__ __forceinline__ void fence_proxy_async() {

@@ -445,8 +445,14 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         }
     }
     // 4-byte summary of all per-query statuses
-    uint32_t hflags = 0;
-    e = cudaMemcpyAsync(&hflags, d_flags, 4, cudaMemcpyDeviceToHost, s);
+    // the 4-byte status summary lands in a pinned word of the handle: a copy
+    // into pageable memory would stage through the driver and stall the call
+    if (!h->host_flags) {
+        e = cudaMallocHost(&h->host_flags, 16);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMallocHost(flags)");
+    }
+    h->host_flags[0] = 0;
+    e = cudaMemcpyAsync(h->host_flags, d_flags, 4, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_status(e, "D2H(flags)");
     const bool counters = out_qctr != nullptr || (stats && !(opts && opts->timing_only));
     std::vector<uint32_t> ctr_host;
@@ -460,6 +466,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     if (e != cudaSuccess) return cuda_status(e, "search");
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "search");
+    uint32_t hflags = h->host_flags[0];
 
     // Queries whose shared-memory tie stack overflowed are re-run at once with
     // the stack in global memory (capacity n: a node enters it at most once),
@@ -522,13 +529,13 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
                         e = cudaMemcpyAsync(o->user, o->dev, o->bytes, cudaMemcpyDeviceToHost, s);
                         if (e != cudaSuccess) break;
                     }
-                uint32_t rflags = 0;
+                h->host_flags[1] = 0;
                 if (e == cudaSuccess && st == QVG_OK)
-                    e = cudaMemcpyAsync(&rflags, d_flags, 4, cudaMemcpyDeviceToHost, s);
+                    e = cudaMemcpyAsync(h->host_flags + 1, d_flags, 4, cudaMemcpyDeviceToHost, s);
                 if (e == cudaSuccess && st == QVG_OK && stats && counters && !o_ctr.copy_back)
                     e = cudaMemcpyAsync(ctr_host.data(), o_ctr.dev, nq * 32, cudaMemcpyDeviceToHost, s);
                 if (e == cudaSuccess && st == QVG_OK) e = cudaStreamSynchronize(s);
-                hflags = (hflags & ~(1u << QVG_Q_TIE_OVERFLOW)) | rflags;
+                hflags = (hflags & ~(1u << QVG_Q_TIE_OVERFLOW)) | h->host_flags[1];
             }
             cudaFree(spill);
             cudaFree(qmap);

@@ -405,8 +405,12 @@ void launch_encode(const float* x, uint64_t nq, uint32_t dim, uint32_t Dp, float
         }
         if (qb) {
             const size_t lsmem = row_bytes * qb;
-            cudaFuncSetAttribute(encode_lpq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lsmem);
+            static size_t lpq_attr = 0;  // attribute calls cost host time on small batches
+            if (lsmem > lpq_attr) {
+                cudaFuncSetAttribute(encode_lpq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(200u * 1024u));
+                lpq_attr = 200u * 1024u;
+            }
             const unsigned blocks = (unsigned)((nq + qb - 1) / qb);
             encode_lpq_kernel<<<blocks, kLpqThreads, lsmem, s>>>(x, nq, dim, Dp, qb, qn, qcodes,
                                                                  tau, status, flags);

@@ -84,6 +84,7 @@ void free_index(qvg_index* h) {
     if (h->ev_copy) cudaEventDestroy(h->ev_copy);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->ready_host) cudaFreeHost(h->ready_host);
+    if (h->host_flags) cudaFreeHost(h->host_flags);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }

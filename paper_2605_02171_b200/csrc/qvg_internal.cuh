@@ -65,6 +65,7 @@ struct qvg_index {
     cudaEvent_t ev_copy = nullptr;
     uint32_t* ready_host = nullptr;
     size_t ready_cap = 0;
+    uint32_t* host_flags = nullptr;  // pinned: per-call status summary (D2H target)
     // TMA descriptor over the code rows (2-D: 2W u64 columns x n rows, box
     // {2W, 1}) for tile::gather4; valid iff has_tmap (W <= 128)
     alignas(64) CUtensorMap tmap;
@@ -161,7 +162,7 @@ qvg_status launch_search(const SearchLaunch& a, const CUtensorMap* tmap, uint64_
 // latency mode (search_coop.cu): one CTA of warps per query for small batches
 uint64_t coop_capacity(const SearchLaunch& a, int device);  // 0 = not applicable
 // (grid_out: the CTAs launched; stats report them with warps_per_block = kCoopWarps)
-constexpr int kCoopWarps = 4;
+constexpr int kCoopWarps = 8;  // 1 leader + 7 helper warps
 qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s, int device,
                        uint64_t* grid_out = nullptr);
 // encode the gather4 descriptor for a code table (false if W > 128)

@@ -4,13 +4,18 @@
 // right trade when thousands of queries keep every SM busy; with a handful of
 // queries the GPU is idle and a query's latency is its serial chain of ~80
 // expansions.  Here the per-expansion work that parallelises is spread over
-// the CTA:
-//   * every warp TMA-gathers and scores its slice of the expansion's rows
-//     (<= 16 of 64) in one round trip, into a shared distance array;
-//   * the leader warp then runs the unchanged state machine of search.cu —
-//     the same contender test, prefix admission, in-place merge, tie stack,
-//     pick, visited table and compaction, on the same distances in the same
-//     row order — so pools, ids and scores are identical (search.cpp:27-81);
+// the CTA, and the leader's bookkeeping is taken off the memory round trip:
+//   * three helper warps TMA-gather and score a third of the expansion's rows
+//     each (<= 24 of 64) in one round trip, into a shared distance array, and
+//     copy the adjacency row of their slice's smallest row in the background;
+//   * the leader warp runs the unchanged state machine of search.cu — the same
+//     contender test, prefix admission, in-place merge, tie stack, pick,
+//     visited table and compaction, on the same distances in the same row
+//     order — so pools, ids and scores are identical (search.cpp:27-81).  It
+//     takes the next pick right after the contender test (min of the predicted
+//     pick and the smallest contender, which is always admitted), publishes its
+//     surviving neighbours, and merges the contenders while the helpers already
+//     gather the next rows;
 //   * the rerank spreads the pool over all lanes, four lanes per row: lane c
 //     accumulates chain c (elements i = c mod 4, ascending) and lane 0 of the
 //     group folds the tail and combines (s0 + s1) + (s2 + s3) — the reference's
@@ -21,6 +26,8 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "bq_device.cuh"
 #include "qvg_internal.cuh"
@@ -30,9 +37,26 @@ namespace qvg {
 
 namespace {
 
+// per-phase cycle counters (variant build: build.py --variant cphases -DQVG_COOP_PHASES)
+#ifdef QVG_COOP_PHASES
+#define QVG_CP(...) __VA_ARGS__
+// per-step event timestamps (SM clock cycles) of the block serving query 0:
+// [step][event]; events: 0 step start (leader), 1 leader phase C done, 2 S1
+// passed (leader), 3 combine done, 4 adjacency row ready, 5 filter done,
+// 8 helper 0 step start, 9 gather landed, 10 scored, 11 bar 1 passed,
+// 12 contender test done
+__device__ unsigned long long g_coop_trace[1024][16];
+__device__ __forceinline__ void coop_ev(uint64_t q, uint32_t iter_q, int ev) {
+    if (q != 0 || iter_q >= 1024 || (threadIdx.x & 31) != 0) return;
+    g_coop_trace[iter_q][ev] = (unsigned long long)clock64();  // one SM: one clock
+}
+#else
+#define QVG_CP(...)
+#endif
+
 struct CoopLayout {
-    uint32_t bars, stages, stage_bytes, pk, ctd, evk, crp, csrp, cid, stg, dsh, spec, qc, tie, vis,
-        qn, ctl, total;
+    uint32_t bars, stages, stage_bytes, pk, ctd, evk, crp, csrp, cid, stg, dsh, spec, smin, scop, hctd,
+        hcrp, hcnt, hdrop, qc, tie, vis, qn, ctl, total;
 };
 
 // block carve-up; SRW = rows per warp (multiple of 4)
@@ -47,9 +71,9 @@ __host__ __device__ inline CoopLayout coop_layout(uint32_t EFM, uint32_t RM, uin
         o += bytes;
         return at;
     };
-    L.bars = take(8 * kCoopWarps, 16);
+    L.bars = take(8 * 2 * kCoopWarps, 16);         // gather + adjacency mbarrier per helper
     L.stage_bytes = (SRW / 4) * group_stride(W);  // multiple of 128
-    L.stages = take(kCoopWarps * L.stage_bytes, 128);
+    L.stages = take((kCoopWarps - 1) * L.stage_bytes, 128);  // helpers only
     L.pk = take(8 * EFM, 16);
     L.ctd = take(8 * RM, 16);
     L.evk = L.ctd;
@@ -58,12 +82,23 @@ __host__ __device__ inline CoopLayout coop_layout(uint32_t EFM, uint32_t RM, uin
     L.cid = take(4 * RM, 16);
     L.stg = L.crp;
     L.dsh = take(4 * RM, 16);     // row distances, row order
-    L.spec = take(4 * RM, 16);    // predicted next pick's adjacency row (L2 prefetch)
+    // per helper: the adjacency row of its slice's smallest (dist, id) row,
+    // bulk-copied in the background (the next pick whenever a contender beats
+    // the predicted one), and that row's key
+    L.spec = take((kCoopWarps - 1) * 4 * RM, 16);
+    L.smin = take((kCoopWarps - 1) * 8, 16);
+    L.scop = take((kCoopWarps - 1) * 8, 16);  // key whose adjacency row was copied
+    // per helper: its slice's contenders (keys, ranks in P, row order), count,
+    // and visited-table-miss drops
+    L.hctd = take((kCoopWarps - 1) * 8 * SRW, 16);
+    L.hcrp = take((kCoopWarps - 1) * 4 * SRW, 16);
+    L.hcnt = take((kCoopWarps - 1) * 4, 16);
+    L.hdrop = take((kCoopWarps - 1) * 4, 16);
     L.qc = take(16 * W, 16);
     L.tie = take(4 * tie_cap, 16);
     L.vis = take(4 * vis_slots, 16);  // rerank scores alias it (vis_slots >= EFM)
     L.qn = take(4 * Dp, 16);          // normalised query (rerank)
-    L.ctl = take(32, 16);             // query index (u64), row count, done flag
+    L.ctl = take(32, 16);             // query index (u64), row count, done flag, np, guess key
     L.total = (o + 127u) & ~127u;
     return L;
 }
@@ -84,8 +119,11 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
     const uint32_t EFM = (ef + 31u) & ~31u;
     const CoopLayout L = coop_layout(EFM, RM, W, a.tie_cap, VS, ix.Dp, SRW);
     unsigned char* base = smem_raw;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bars) + w;
-    unsigned char* const stage = base + L.stages + w * L.stage_bytes;
+    // helper h = w - 1 gathers and scores rows [h*SRW, (h+1)*SRW) of an expansion
+    const uint32_t h = w - 1;  // (meaningless for the leader, w == 0)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bars) + (w ? h : 0);
+    uint64_t* abar = reinterpret_cast<uint64_t*>(base + L.bars) + kCoopWarps;  // [helper]
+    unsigned char* const stage = base + L.stages + (w ? h : 0) * L.stage_bytes;
     uint64_t* pk = reinterpret_cast<uint64_t*>(base + L.pk);
     uint64_t* ctd = reinterpret_cast<uint64_t*>(base + L.ctd);
     uint64_t* evk = reinterpret_cast<uint64_t*>(base + L.evk);
@@ -94,7 +132,13 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
     uint32_t* cid = reinterpret_cast<uint32_t*>(base + L.cid);
     uint32_t* stg = reinterpret_cast<uint32_t*>(base + L.stg);
     uint32_t* dsh = reinterpret_cast<uint32_t*>(base + L.dsh);
-    uint32_t* spec = reinterpret_cast<uint32_t*>(base + L.spec);
+    uint32_t* adjw = reinterpret_cast<uint32_t*>(base + L.spec);  // [helper][RM]
+    uint64_t* smin = reinterpret_cast<uint64_t*>(base + L.smin);  // [helper]
+    uint64_t* scop = reinterpret_cast<uint64_t*>(base + L.scop);  // [helper]
+    uint64_t* hctd = reinterpret_cast<uint64_t*>(base + L.hctd);  // [helper][SRW]
+    uint32_t* hcrp = reinterpret_cast<uint32_t*>(base + L.hcrp);  // [helper][SRW]
+    uint32_t* hcnt = reinterpret_cast<uint32_t*>(base + L.hcnt);  // [helper]
+    uint32_t* hdrop = reinterpret_cast<uint32_t*>(base + L.hdrop);  // [helper]
     uint4* qc = reinterpret_cast<uint4*>(base + L.qc);
     uint32_t* tie = reinterpret_cast<uint32_t*>(base + L.tie);
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
@@ -103,12 +147,18 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
     unsigned long long* ctl_q = reinterpret_cast<unsigned long long*>(base + L.ctl);
     volatile uint32_t* ctl_n = reinterpret_cast<volatile uint32_t*>(base + L.ctl + 8);
     volatile uint32_t* ctl_done = reinterpret_cast<volatile uint32_t*>(base + L.ctl + 12);
+    // pool size published by the leader for the helpers' contender tests
+    volatile uint32_t& np_sh = *reinterpret_cast<volatile uint32_t*>(base + L.ctl + 16);
+    // the predicted pick's key, published with it
+    volatile uint64_t& gkey_sh = *reinterpret_cast<volatile uint64_t*>(base + L.ctl + 24);
 
-    if (lane == 0) {
+    if (w > 0 && lane == 0) {
         mbar_init(bar);
+        mbar_init(abar + h);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     uint32_t phase = 0;
+    uint32_t iter = 0;  // expansions issued by this block (adjacency mbarrier parity)
     // lanes per row for this warp's slice (SRW rows): largest 2^k with 2^k*SRW <= 32
     uint32_t lpr_log = 0;
     while ((SRW << (lpr_log + 1)) <= 32u) ++lpr_log;
@@ -168,117 +218,123 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
         __syncthreads();
 
         // ---- best-first loop ------------------------------------------------------
+        // Iteration i: the helpers gather and score the rows of expansion i
+        // (phase A) while the leader finishes expansion i-1's bookkeeping —
+        // rank / merge / tie stack / expanded mark, then the speculative scan
+        // for the next pick (phase C).  Once the leader signals the pool final
+        // (named barrier 1), each helper runs the contender test of its rows
+        // against it and keeps its contenders in row order, their smallest key,
+        // and a background copy of that node's adjacency row.  After the block
+        // barrier the leader concatenates the slices, takes the next pick —
+        // min(predicted pick, smallest contender: always admitted), or the top
+        // of the tie stack — and compacts its surviving neighbours (phase B);
+        // the merge of these contenders is left for phase C of the next
+        // iteration, where it overlaps the next gather.  Same state machine and
+        // the same order of every decision as search.cu (search.cpp:27-81).
+        uint32_t guess_idx = kSentinel;  // predicted pick's index in P
+        uint64_t spec_key = kInfKey;     // its key (then lowered to the pick's)
+        uint32_t pend_m = 0;             // contenders of the last expansion, to merge
+        bool pend_pick = false;          // the last pick came from P: mark it expanded
+        uint32_t h_drop = 0;             // helper: visited-table misses dropped
+        QVG_CP(uint32_t it_q = 0;)
         for (;;) {
+            QVG_CP(coop_ev(q, it_q, w == 0 ? 0 : (w == 1 ? 8 : 15));)
             const uint32_t n = *ctl_n;
-            // (a) this warp's slice of the rows: one gather, one round trip
-            const uint32_t r0 = w * SRW;
-            const uint32_t cnt = n > r0 ? min(SRW, n - r0) : 0u;
-            if (cnt) {
-                const uint32_t ng = (cnt + 3u) >> 2;
-                TMA_WAR_FENCE();
-                __syncwarp();
-                if (lane == 0) mbar_expect_tx(bar, ng * 4u * rowb);
-                __syncwarp();
-                if (lane < ng) {
-                    const uint32_t j = r0 + 4u * lane;
-                    const uint32_t i0 = cid[j];
-                    const uint32_t i1 = 4u * lane + 1u < cnt ? cid[j + 1] : i0;
-                    const uint32_t i2 = 4u * lane + 2u < cnt ? cid[j + 2] : i0;
-                    const uint32_t i3 = 4u * lane + 3u < cnt ? cid[j + 3] : i0;
-                    dev::tma_gather4(stage + lane * gstride, &tmap, 0, i0, i1, i2, i3, bar);
-                }
-            }
-            if (w == 0) {  // speculative adjacency of the current best unexpanded entry
-                uint32_t guess = kSentinel;
-                for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
-                    const uint32_t idx = b0 + lane;
-                    const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
-                    const unsigned bal = __ballot_sync(kFull, un);
-                    if (bal) {
-                        guess = (uint32_t)pk[b0 + __ffs(bal) - 1];
-                        break;
-                    }
-                }
-                if (guess == kSentinel && tn > 0) guess = tie[tn - 1];
-                spec_u = guess;
-                if (guess != kSentinel) {
-                    const uint32_t* row = ix.adj + (size_t)guess * ix.RS;
-                    if (lane * RW < ix.RS) {
-                        if (RW == 1) {
-                            spec_v[0] = __ldg(row + lane);
-                        } else if (RW == 2) {
-                            const uint2 t = __ldg(reinterpret_cast<const uint2*>(row) + lane);
-                            spec_v[0] = t.x;
-                            spec_v[RW - 1] = t.y;
-                        } else {
-                            const uint4 t = __ldg(reinterpret_cast<const uint4*>(row) + lane);
-                            spec_v[0] = t.x;
-                            spec_v[1 % RW] = t.y;
-                            spec_v[2 % RW] = t.z;
-                            spec_v[3 % RW] = t.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < RW; ++j) spec_v[j] = kSentinel;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < RW; ++j)  // published for the helpers' L2 prefetch
-                    spec[lane * RW + j] = guess != kSentinel ? spec_v[j] : kSentinel;
-            }
-            if (cnt) {
-                mbar_wait(bar, phase);
-                phase ^= 1u;
-                const uint4* st = reinterpret_cast<const uint4*>(stage);
-                const uint32_t j = lane >> lpr_log;
-                const uint32_t part = lane & (LPR - 1u);
-                uint32_t d = 0;
-                if (j < cnt) {
-                    const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
-                    d = row_sm2(qc, rowp, W, rot, part, LPR);
-                }
-                for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
-                if (j < cnt && part == 0) dsh[r0 + j] = d;
-            }
-            __syncthreads();  // all slices scored
-
             if (w > 0) {
-                // helpers are idle while the leader merges: warm L2 with the code
-                // rows of the predicted next pick (its rows are gathered next
-                // whenever the prediction holds)
-                for (uint32_t sl = (w - 1) * 32 + lane; sl < RM; sl += (kCoopWarps - 1) * 32) {
-                    const uint32_t id = spec[sl];
-                    if (id != kSentinel) prefetch_l2(ix.codes + (size_t)id * W, rowb);
+                // ---- phase A (helpers): gather + score this helper's slice
+                const uint32_t r0 = h * SRW;
+                const uint32_t cnt = n > r0 ? min(SRW, n - r0) : 0u;
+                uint64_t rmin = kInfKey;  // the slice's smallest scored key
+                if (cnt) {
+                    const uint32_t ng = (cnt + 3u) >> 2;
+                    TMA_WAR_FENCE();
+                    __syncwarp();
+                    if (lane == 0) mbar_expect_tx(bar, ng * 4u * rowb);
+                    __syncwarp();
+                    for (uint32_t g = lane; g < ng; g += 32) {
+                        const uint32_t j = r0 + 4u * g;
+                        const uint32_t i0 = cid[j];
+                        const uint32_t i1 = 4u * g + 1u < cnt ? cid[j + 1] : i0;
+                        const uint32_t i2 = 4u * g + 2u < cnt ? cid[j + 2] : i0;
+                        const uint32_t i3 = 4u * g + 3u < cnt ? cid[j + 3] : i0;
+                        dev::tma_gather4(stage + g * gstride, &tmap, 0, i0, i1, i2, i3, bar);
+                    }
+                    mbar_wait(bar, phase);
+                    phase ^= 1u;
+                    QVG_CP(if (w == 1) coop_ev(q, it_q, 9);)
+                    const uint4* st = reinterpret_cast<const uint4*>(stage);
+                    const uint32_t part = lane & (LPR - 1u);
+                    for (uint32_t j0 = 0; j0 < cnt; j0 += 32u >> lpr_log) {
+                        const uint32_t j = j0 + (lane >> lpr_log);
+                        uint32_t d = 0;
+                        if (j < cnt) {
+                            const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
+                            d = row_sm2(qc, rowp, W, rot, part, LPR);
+                        }
+                        for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
+                        const bool lead = j < cnt && part == 0;
+                        if (lead) dsh[r0 + j] = d;
+                        const uint32_t id = lead ? cid[r0 + j] : ~0u;
+                        const uint32_t dm = __reduce_min_sync(kFull, lead ? d : ~0u);
+                        const uint32_t im = __reduce_min_sync(kFull, (lead && d == dm) ? id : ~0u);
+                        if (dm != ~0u && mkkey(dm, im) < rmin) rmin = mkkey(dm, im);
+                    }
                 }
-            }
-            if (w == 0) {
-                c_eval += n;
-                const uint64_t worst = np == ef ? ordk(pk[ef - 1]) : kInfKey;
+                QVG_CP(if (w == 1) coop_ev(q, it_q, 10);)
+                // background copy of the adjacency row of the slice's smallest
+                // row, issued before the contender test: whenever the next pick
+                // is a contender that beats the prediction it is the smallest
+                // contender, almost always the smallest row of its slice.  One
+                // copy per iteration keeps the mbarrier parity = iter & 1.
+                if (lane == 0) {
+                    if (iter > 0) mbar_wait(abar + h, (iter - 1) & 1u);  // buffer / barrier free
+                    scop[h] = rmin;
+                    const uint32_t src = rmin != kInfKey ? (uint32_t)rmin : a.entry;
+                    mbar_expect_tx(abar + h, 4u * ix.RS);
+                    bulk_row(adjw + h * RM, ix.adj + (size_t)src * ix.RS, 4u * ix.RS, abar + h);
+                }
+                __syncwarp();
+                // contender test of the slice against the final pool
+                asm volatile("bar.sync 1, %0;" ::"r"(kCoopWarps * 32) : "memory");
+                QVG_CP(if (w == 1) coop_ev(q, it_q, 11);)
+                const uint64_t worst = np_sh == ef ? ordk(pk[ef - 1]) : kInfKey;
+                const uint32_t npv = np_sh;
                 uint32_t m = 0;
-                // (b) contender test + row-order compaction
-                for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+                uint64_t kmin = kInfKey;
+                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
                     const uint32_t jr = i0 + lane;
-                    const bool valid = jr < n;
-                    const uint64_t key = valid ? mkkey(dsh[jr], cid[jr]) : kInfKey;
+                    const bool valid = jr < cnt;
+                    const uint64_t key = valid ? mkkey(dsh[r0 + jr], cid[r0 + jr]) : kInfKey;
                     bool c = valid && key < worst;
                     uint32_t rp = 0;
                     if (c) {
-                        rp = lower_bound_key(pk, np, key);
-                        if (rp < np && ordk(pk[rp]) == key) {
+                        rp = lower_bound_key(pk, npv, key);
+                        if (rp < npv && ordk(pk[rp]) == key) {
                             c = false;  // already pooled (visited-table miss)
-                            ++c_drop;
+                            ++h_drop;
                         }
                     }
                     const unsigned bal = __ballot_sync(kFull, c);
                     if (c) {
                         const uint32_t pos = m + __popc(bal & lt_mask);
-                        ctd[pos] = key;
-                        crp[pos] = rp;
+                        hctd[h * SRW + pos] = key;
+                        hcrp[h * SRW + pos] = rp;
                     }
                     m += __popc(bal);
+                    const uint32_t dm = __reduce_min_sync(kFull, c ? kdist(key) : ~0u);
+                    const uint32_t im = __reduce_min_sync(kFull, (c && kdist(key) == dm) ? (uint32_t)key : ~0u);
+                    if (dm != ~0u && mkkey(dm, im) < kmin) kmin = mkkey(dm, im);
                 }
-                __syncwarp();
-                if (m > 0) {
+                if (lane == 0) {
+                    hcnt[h] = m;
+                    smin[h] = kmin;  // the slice's smallest contender
+                }
+                QVG_CP(if (w == 1) coop_ev(q, it_q, 12);)
+            } else {
+                // ---- phase C (leader) of the previous expansion
+                uint32_t ins_lo = kSentinel;
+                if (pend_m > 0) {
+                    const uint32_t m = pend_m;
                     // (c) contender ranks (key order) and prefix counts (row order)
                     uint64_t y[RW];
                     uint32_t rk[RW], pre[RW], rpv[RW];
@@ -305,6 +361,7 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                     __syncwarp();
                     // (d) in-place merge of P's tail, backwards
                     const uint32_t lo = csrp[0];
+                    ins_lo = lo;
                     const uint32_t total = np + m;
                     if (lo < np) {
                         for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
@@ -367,72 +424,154 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                     np = total < ef ? total : ef;
                     __syncwarp();
                 }
-                // (f) pick
-                uint32_t u = kSentinel;
+                // (f') the last pick's expanded mark at its index in P': entries
+                // before the first insertion point are unchanged, so it is the
+                // predicted pick's index unless the smallest contender came first
+                if (pend_pick) {
+                    const uint32_t pick = ins_lo < guess_idx ? ins_lo : guess_idx;
+                    __syncwarp();
+                    if (lane == 0) pk[pick] = spec_key | kExp;
+                    hint = pick + 1;
+                }
+                // speculative scan: the best unexpanded entry of the pool (the
+                // next pick unless a contender of this expansion beats it)
+                uint32_t guess = kSentinel;
+                guess_idx = kSentinel;
+                spec_key = kInfKey;
                 for (uint32_t b0 = hint & ~31u; b0 < np; b0 += 32) {
                     const uint32_t idx = b0 + lane;
-                    const bool un = idx < np && idx >= hint && !(pk[idx] & kExp);
+                    const uint64_t pv = idx < np ? pk[idx] : kExp;
+                    const bool un = idx >= hint && !(pv & kExp);
                     const unsigned bal = __ballot_sync(kFull, un);
                     if (bal) {
-                        const uint32_t pick = b0 + __ffs(bal) - 1;
-                        u = (uint32_t)pk[pick];
-                        __syncwarp();
-                        if (lane == 0) pk[pick] |= kExp;
-                        hint = pick + 1;
+                        const uint32_t src = __ffs(bal) - 1;
+                        guess_idx = b0 + src;
+                        spec_key = __shfl_sync(kFull, pv, src);
+                        guess = (uint32_t)spec_key;
                         break;
                     }
                 }
-                bool done = false;
-                if (u == kSentinel) {
-                    hint = np;
-                    if (tn == 0) {
-                        done = true;
-                    } else {
-                        u = tie[tn - 1];
-                        --tn;
-                        ++c_tie;
+                if (guess == kSentinel && tn > 0) guess = tie[tn - 1];
+                spec_u = guess;
+                if (lane == 0) {
+                    np_sh = np;
+                    gkey_sh = spec_key;
+                }
+                __syncwarp();
+                // the pool is final for this expansion's contender tests
+                asm volatile("bar.arrive 1, %0;" ::"r"(kCoopWarps * 32) : "memory");
+                // the predicted pick's adjacency row, and its neighbours' code
+                // rows warmed in L2 (the next gather whenever the prediction holds)
+                if (guess != kSentinel) {
+#pragma unroll
+                    for (int j = 0; j < RW; ++j) {
+                        const uint32_t sl = lane * RW + j;
+                        spec_v[j] = sl < ix.RS ? __ldg(ix.adj + (size_t)guess * ix.RS + sl) : kSentinel;
+                    }
+#pragma unroll
+                    for (int j = 0; j < RW; ++j)
+                        if (spec_v[j] != kSentinel)
+                            prefetch_lines_l2(ix.codes + (size_t)spec_v[j] * W, rowb);
+                }
+                QVG_CP(coop_ev(q, it_q, 1);)
+            }
+            __syncthreads();  // S1: this expansion's contenders found, P final
+            QVG_CP(if (w == 0) coop_ev(q, it_q, 2);)
+            if (w > 0) {
+                // while the leader picks: a slice whose smallest contender beats
+                // the prediction holds a likely next pick — warm L2 with its
+                // neighbours' code rows (its adjacency row is the background copy)
+                const uint64_t km = smin[h];
+                if (km < gkey_sh && scop[h] == km) {
+                    mbar_wait(abar + h, iter & 1u);
+                    for (uint32_t sl = lane; sl < ix.RS; sl += 32) {
+                        const uint32_t id = adjw[h * RM + sl];
+                        if (id != kSentinel) prefetch_lines_l2(ix.codes + (size_t)id * W, rowb);
                     }
                 }
-                if (done) {
+            }
+
+            if (w == 0) {
+                // ---- phase B (leader): the helpers' contenders in row order
+                c_eval += n;
+                uint32_t off[kCoopWarps - 1];
+                uint32_t m = 0;
+                uint64_t kmin = kInfKey;
+                int hsrc = -1;
+#pragma unroll
+                for (int hh = 0; hh < kCoopWarps - 1; ++hh) {
+                    off[hh] = m;
+                    m += hcnt[hh];
+                    const uint64_t km = smin[hh];
+                    if (km < kmin) {
+                        kmin = km;
+                        hsrc = hh;
+                    }
+                }
+                for (uint32_t i = lane; i < m; i += 32) {
+                    uint32_t k2 = i;  // slot in the helper segments (constant indices only:
+#pragma unroll                        // a runtime index would put off[] in local memory)
+                    for (int t = 1; t < kCoopWarps - 1; ++t)
+                        if (i >= off[t]) k2 = t * SRW + (i - off[t]);
+                    ctd[i] = hctd[k2];
+                    crp[i] = hcrp[k2];
+                }
+                __syncwarp();
+                QVG_CP(coop_ev(q, it_q, 3);)
+                // (f) pick: the smallest contender is always admitted, so the
+                // best unexpanded entry of P' is min(predicted pick, kmin); with
+                // none, the top of the tie stack (m == 0 then: the stack is final)
+                uint32_t u = kSentinel;
+                bool from_p = false;
+                const bool retarget = kmin < spec_key;
+                if (retarget) spec_key = kmin;
+                if (spec_key != kInfKey) {
+                    u = (uint32_t)spec_key;
+                    from_p = true;
+                } else if (tn > 0) {
+                    u = tie[tn - 1];
+                    --tn;
+                    ++c_tie;
+                    hint = np;
+                }
+                pend_m = m;
+                pend_pick = from_p;
+                if (u == kSentinel) {
                     if (lane == 0) *ctl_done = 1;
                 } else {
                     ++c_exp;
-                    // (g) adjacency row (speculative hit or fresh load)
+                    // (g) adjacency row: the predicted pick's (loaded in phase
+                    // C), else the background copy of the winning slice's
                     uint32_t v[RW];
-                    if (u == spec_u) {
+                    if (!retarget && u == spec_u) {
 #pragma unroll
                         for (int j = 0; j < RW; ++j) v[j] = spec_v[j];
-                    } else {
-                        const uint32_t* row = ix.adj + (size_t)u * ix.RS;
-                        if (lane * RW < ix.RS) {
-                            if (RW == 1) {
-                                v[0] = __ldg(row + lane);
-                            } else if (RW == 2) {
-                                const uint2 t = __ldg(reinterpret_cast<const uint2*>(row) + lane);
-                                v[0] = t.x;
-                                v[RW - 1] = t.y;
-                            } else {
-                                const uint4 t = __ldg(reinterpret_cast<const uint4*>(row) + lane);
-                                v[0] = t.x;
-                                v[1 % RW] = t.y;
-                                v[2 % RW] = t.z;
-                                v[3 % RW] = t.w;
-                            }
-                        } else {
+                    } else if (scop[hsrc] == kmin) {
+                        mbar_wait(abar + hsrc, iter & 1u);
 #pragma unroll
-                            for (int j = 0; j < RW; ++j) v[j] = kSentinel;
+                        for (int j = 0; j < RW; ++j) {
+                            const uint32_t sl = lane * RW + j;
+                            v[j] = sl < ix.RS ? adjw[hsrc * RM + sl] : kSentinel;
+                        }
+                    } else {  // the slice's smallest row was no contender (rare)
+#pragma unroll
+                        for (int j = 0; j < RW; ++j) {
+                            const uint32_t sl = lane * RW + j;
+                            v[j] = sl < ix.RS ? __ldg(ix.adj + (size_t)u * ix.RS + sl) : kSentinel;
                         }
                     }
-                    // (h) visited filter + compaction
+                    QVG_CP(coop_ev(q, it_q, 4);)
+                    // (h) visited filter + compaction (the helpers have read
+                    // this expansion's cid)
                     bool keep[RW];
 #pragma unroll
                     for (int j = 0; j < RW; ++j) {
                         const uint32_t id = v[j];
                         bool k2 = id != kSentinel;
                         if (k2) {
-                            const uint32_t s = vhash(id, a.vis_log2);
-                            if (vis[s] == id) k2 = false;
-                            else vis[s] = id;
+                            const uint32_t sidx = vhash(id, a.vis_log2);
+                            if (vis[sidx] == id) k2 = false;
+                            else vis[sidx] = id;
                         }
                         keep[j] = k2;
                     }
@@ -450,15 +589,23 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                     for (int j = 0; j < RW; ++j)
                         if (keep[j]) cid[pos++] = v[j];
                     if (lane == 0) *ctl_n = nn;
+                    QVG_CP(coop_ev(q, it_q, 5);)
                 }
+                fence_proxy_async();  // adjw reads before the helpers' next bulk copies
             }
-            __syncthreads();  // next rows (or done) published
+            ++iter;
+            __syncthreads();  // F1: next rows published (or done)
+            QVG_CP(++it_q;)
             if (*ctl_done) break;
         }
+        if (w > 0 && lane == 0) hdrop[h] = h_drop;
+        // every helper's last background copy has landed before smem is reused
+        if (w > 0 && lane == 0 && iter > 0) mbar_wait(abar + h, (iter - 1) & 1u);
 
         // ---- outputs (leader) --------------------------------------------------------
+        __syncthreads();  // the helpers' drop counts
         if (w == 0) {
-            for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
+            for (int hh = 0; hh < kCoopWarps - 1; ++hh) c_drop += hdrop[hh];
             if (a.pool_ids) {
                 for (uint32_t i = lane; i < ef; i += 32) {
                     a.pool_ids[q * ef + i] = i < np ? (uint32_t)pk[i] : kSentinel;
@@ -560,13 +707,46 @@ CoopPlan coop_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t 
     p.rw = pow2ceil_c((ix.R + 31) / 32);
     p.fn = p.rw == 1 ? (void*)coop_kernel<1> : (p.rw == 2 ? (void*)coop_kernel<2> : (void*)coop_kernel<4>);
     const uint32_t RM = p.rw * 32;
-    p.SRW = (((RM + kCoopWarps - 1) / kCoopWarps) + 3u) & ~3u;  // <= 32 rows per warp
+    // rows per helper warp (the leader scores none): a multiple of 4
+    p.SRW = (((RM + kCoopWarps - 2) / (kCoopWarps - 1)) + 3u) & ~3u;
     p.block_bytes =
         coop_layout((ef + 31) & ~31u, RM, ix.W, tie_cap, 1u << vis_log2, ix.Dp, p.SRW).total;
     return p;
 }
 
 }  // namespace
+
+// resident CTAs per SM of a coop instantiation at a shared-memory size, cached
+// (the occupancy query and the attribute call cost host time on every small-
+// batch call, where the GPU would otherwise wait for the launch)
+static int coop_per_sm(void* fn, uint32_t block_bytes, int device) {
+    struct Key {
+        void* fn;
+        uint32_t bytes;
+        int dev;
+        bool operator<(const Key& o) const {
+            if (fn != o.fn) return fn < o.fn;
+            return bytes != o.bytes ? bytes < o.bytes : dev < o.dev;
+        }
+    };
+    static std::mutex mu;
+    static std::map<Key, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const Key k{fn, block_bytes, device};
+    auto it = cache.find(k);
+    if (it != cache.end()) return it->second;
+    int maxs = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (block_bytes > (uint32_t)maxs ||
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCoopWarps * 32, block_bytes) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 0;
+    }
+    cache.emplace(k, per_sm);
+    return per_sm;
+}
 
 // resident CTAs (= concurrently served queries) of the latency kernel for
 // this launch, 0 when it cannot run it
@@ -576,31 +756,24 @@ uint64_t coop_capacity(const SearchLaunch& a, int device) {
     if (extra_depth(a.ef, a.depth)) return 0;
     if ((1u << a.vis_log2) < ((a.ef + 31u) & ~31u)) return 0;
     const CoopPlan p = coop_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
-    int maxs = 0, sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (p.block_bytes > (uint32_t)maxs) return 0;
-    if (cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs) !=
-            cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.fn, kCoopWarps * 32,
-                                                      p.block_bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return (uint64_t)per_sm * sms;
+    return (uint64_t)coop_per_sm(p.fn, p.block_bytes, device) * sms;
 }
 
 qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStream_t s,
                        int device, uint64_t* grid_out) {
     const CoopPlan p = coop_plan(a.ix, a.ef, a.vis_log2, a.tie_cap);
-    int maxs = 0, sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaError_t e = cudaFuncSetAttribute(p.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
-    if (e != cudaSuccess) return cuda_status(e, "coop: smem attribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p.fn, kCoopWarps * 32,
-                                                      p.block_bytes);
-    if (e != cudaSuccess || per_sm < 1) return cuda_status(e, "coop: occupancy");
+    static int sms = [device] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+        return v;
+    }();
+    const int per_sm = coop_per_sm(p.fn, p.block_bytes, device);
+    if (per_sm < 1) {
+        set_error("coop: the latency kernel does not fit");
+        return QVG_INVALID_ARGUMENT;
+    }
     uint64_t grid = (uint64_t)per_sm * sms;
     if (a.nq < grid) grid = a.nq;
     if (grid < 1) grid = 1;
@@ -609,9 +782,20 @@ qvg_status launch_coop(const SearchLaunch& a, const CUtensorMap* tmap, cudaStrea
     const CUtensorMap* m = tmap ? tmap : &dummy;
     uint32_t srw = p.SRW;
     void* args[] = {(void*)m, (void*)&a, (void*)&srw};
-    e = cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kCoopWarps * 32), args, p.block_bytes, s);
+    const cudaError_t e =
+        cudaLaunchKernel(p.fn, dim3((unsigned)grid), dim3(kCoopWarps * 32), args, p.block_bytes, s);
     if (grid_out) *grid_out = grid;
     return e == cudaSuccess ? QVG_OK : cuda_status(e, "launch(coop)");
 }
 
 }  // namespace qvg
+
+#ifdef QVG_COOP_PHASES
+// instrumented build only: the trace of query 0's block (tools/coop_phases.py)
+extern "C" int qvg_debug_coop_trace(unsigned long long* out, int rows) {
+    return cudaMemcpyFromSymbol(out, qvg::g_coop_trace, sizeof(unsigned long long) * 16 * rows) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
+#endif

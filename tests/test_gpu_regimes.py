@@ -46,7 +46,7 @@ def _ref_graph(dim):
 def test_latency_kernel_vs_reference(dim, ef):
     """Batch 1 and batch 128 (config 3's latency batches) through the public
     call with host and with device-resident buffers: the launch must be the
-    latency kernel (stats warps_per_block == 4: one 4-warp CTA per query) and
+    latency kernel (stats warps_per_block == 8: one 8-warp CTA per query) and
     every result identical to the reference's."""
     import torch
     ref, ix, q = _ref_graph(dim)
@@ -56,7 +56,7 @@ def test_latency_kernel_vs_reference(dim, ef):
             qs = q[off:off + B]
             # host buffers (qvg_search, the drop-in call)
             ids, sc, cnt, st = ix.search(qs, k=10, ef=ef, stats=True)
-            assert st["warps_per_block"] == 4, (dim, ef, B, st["warps_per_block"])
+            assert st["warps_per_block"] == 8, (dim, ef, B, st["warps_per_block"])
             sl = slice(off, off + B)
             _same(rid[sl], rsc[sl], rcnt[sl], ids, sc, cnt, (dim, ef, B, off, "host"))
             # device-resident queries and outputs
@@ -65,7 +65,7 @@ def test_latency_kernel_vs_reference(dim, ef):
             o_sc = torch.empty((B, 10), dtype=torch.float32, device="cuda")
             o_cnt = torch.empty(B, dtype=torch.int32, device="cuda")
             _, _, _, st = ix.search(qd, k=10, ef=ef, out=(o_ids, o_sc, o_cnt), stats=True)
-            assert st["warps_per_block"] == 4
+            assert st["warps_per_block"] == 8
             _same(rid[sl], rsc[sl], rcnt[sl], o_ids.cpu().numpy().view(np.uint32),
                   o_sc.cpu().numpy(), o_cnt.cpu().numpy().view(np.uint32),
                   (dim, ef, B, off, "device"))
