@@ -213,7 +213,12 @@ typedef struct qvg_build_params {
     uint32_t passes;   /* 1 or 2 */
     uint32_t batch;    /* max insertion batch (0 = 65536) */
     uint64_t seed;     /* insertion-order shuffle */
-    uint32_t reserved[4];
+    uint32_t prune_candidates; /* RobustPrune candidates besides the L-best pool
+                                  (+ the node's row on the 2nd pass): bit 0 / bit 1
+                                  = also Vamana's visited set V (the search's
+                                  expanded nodes) on the first / the final alpha
+                                  pass; 0 = default (3: both passes) */
+    uint32_t reserved[3];
 } qvg_build_params;
 
 typedef struct qvg_build_stats {
@@ -236,7 +241,7 @@ qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim, const qvg_buil
  * at most max_degree kept.  Output: out_ids[t * max_degree ...] (unused slots
  * UINT32_MAX), out_count[t].  The builder's own prune kernel (qvg_build) runs
  * it.  Candidate ids must be distinct within a task (they are at every
- * reference call site); at most 256 per task; 1 <= max_degree <= 128.  All
+ * reference call site); at most 480 per task; 1 <= max_degree <= 128.  All
  * pointers host or device. */
 qvg_status qvg_robust_prune(qvg_index* index, uint64_t ntasks, const uint64_t* offsets,
                             const uint32_t* cand_ids, const uint32_t* cand_dists,

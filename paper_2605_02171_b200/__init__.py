@@ -106,6 +106,7 @@ class BuildParams:
     passes: int = 1
     batch: int = 0
     seed: int = 42
+    prune_candidates: int = 0  # qvg.h: bit0/bit1 = visited set V on the first/final pass
 
 
 def _is_tensor(a):
@@ -196,7 +197,7 @@ class GpuIndex:
         data = _f32(data)
         n, dim = data.shape
         bp = N.qvg_build_params(m=p.m, ef_c=p.ef_c, alpha=p.alpha, passes=p.passes,
-                                batch=p.batch, seed=p.seed)
+                                batch=p.batch, seed=p.seed, prune_candidates=p.prune_candidates)
         bs = N.qvg_build_stats()
         h = C.c_void_p()
         _check(N.lib().qvg_build(N.ptr(data), n, dim, C.byref(bp), device, C.byref(h),

@@ -56,7 +56,7 @@ class qvg_search_opts(C.Structure):
 class qvg_build_params(C.Structure):
     _fields_ = [("m", C.c_uint32), ("ef_c", C.c_uint32), ("alpha", C.c_float),
                 ("passes", C.c_uint32), ("batch", C.c_uint32), ("seed", C.c_uint64),
-                ("reserved", C.c_uint32 * 4)]
+                ("prune_candidates", C.c_uint32), ("reserved", C.c_uint32 * 3)]
 
 
 class qvg_build_stats(C.Structure):

@@ -48,7 +48,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // candidates a prune task holds: the kMaxCand closest by (dist, id) of its
 // existing row and new candidates (streamed in chunks of 32; kCandBuf is the
 // bitonic-sort capacity of kMaxCand + 32 rounded to a power of two)
-constexpr uint32_t kMaxCand = 256;
+constexpr uint32_t kMaxCand = 480;
 constexpr uint32_t kCandBuf = 512;
 
 // ---- stage 0: entry point (builder.cpp:90-120) --------------------------------
@@ -163,6 +163,12 @@ struct PruneArgs {
     // targets may be null (no target: every distance is given)
     uint32_t* out_sel;
     uint32_t* out_cnt;
+    // extra candidates with known distances (the build search's expanded-node
+    // list, Vamana's visited set V): keys dist<<33 | id, ext_n[t] of them at
+    // ext_keys[t * ext_stride ...]; nullable
+    const uint64_t* ext_keys;
+    const uint32_t* ext_n;
+    uint32_t ext_stride;
 };
 
 constexpr int kPruneWarps = 2;
@@ -373,6 +379,23 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
                 nc = kMaxCand;
             }
         }
+        // Vamana's visited set (expanded nodes) as further candidates; a node
+        // also in the pool gives an identical key, dropped after the sort
+        const uint32_t next = a.ext_keys ? a.ext_n[t] : 0u;
+        for (uint32_t i0 = 0; i0 < next; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            if (i < next) {
+                const uint64_t k = a.ext_keys[(size_t)t * a.ext_stride + i];
+                keys[nc + lane] = ((k >> 33) << 32) | (uint32_t)k;
+            }
+            nc += min(32u, next - i0);
+            __syncwarp();
+            if (nc > kMaxCand) {
+                score_unknown(0, nc);
+                sort_keys(nc);
+                nc = kMaxCand;
+            }
+        }
         __syncwarp();
         score_unknown(0, nc);
         sort_keys(nc);
@@ -520,6 +543,12 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
     uint32_t* d_pi = static_cast<uint32_t*>(dalloc((size_t)maxb * L * 4));
     uint32_t* d_pd = static_cast<uint32_t*>(dalloc((size_t)maxb * L * 4));
     uint32_t* d_pn = static_cast<uint32_t*>(dalloc((size_t)maxb * 4));
+    // prune candidates: bit 0 / bit 1 = also the expanded-node list V of the
+    // first / the final (alpha) pass's searches (qvg.h prune_candidates)
+    const uint32_t vmode = p->prune_candidates ? p->prune_candidates : 3u;
+    const uint32_t xcap = 2 * L < kMaxCand ? 2 * L : kMaxCand;
+    uint64_t* d_ex = static_cast<uint64_t*>(dalloc((size_t)maxb * xcap * 8));
+    uint32_t* d_exn = static_cast<uint32_t*>(dalloc((size_t)maxb * 4));
     const size_t npairs = (size_t)maxb * R;
     uint32_t* d_k0 = static_cast<uint32_t*>(dalloc(npairs * 4));
     uint32_t* d_v0 = static_cast<uint32_t*>(dalloc(npairs * 4));
@@ -530,7 +559,7 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
     uint32_t* d_nseg = static_cast<uint32_t*>(dalloc(8));
     unsigned long long* d_ctr = static_cast<unsigned long long*>(dalloc(64));
     if (!d_qc || !d_pi || !d_pd || !d_pn || !d_k0 || !d_v0 || !d_k1 || !d_v1 || !d_fl || !d_seg ||
-        !d_nseg || !d_ctr)
+        !d_nseg || !d_ctr || !d_ex || !d_exn)
         return fail(cuda_status(cudaErrorMemoryAllocation, "qvg_build"));
     size_t sort_bytes = 0, sel_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, d_k0, d_k1, d_v0, d_v1, (int)npairs);
@@ -601,6 +630,10 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
             cudaMemsetAsync(d_ctr, 0, 8, s);
             sa.nq = nb;
             sa.ix = ix;
+            const bool use_v = (vmode >> (pass + 1 == passes ? 1u : 0u)) & 1u;
+            sa.exp_out = use_v ? d_ex : nullptr;
+            sa.exp_n = d_exn;
+            sa.exp_cap = xcap;
             const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
             uint64_t g = (nb + wpb - 1) / wpb;
             if (g > grid_full) g = grid_full;
@@ -620,6 +653,9 @@ extern "C" qvg_status qvg_build(const float* data, uint64_t n, uint32_t dim,
             fa.alpha = alpha;
             fa.R = R;
             fa.reprunes = d_repr;
+            fa.ext_keys = use_v ? d_ex : nullptr;
+            fa.ext_n = d_exn;
+            fa.ext_stride = xcap;
             if ((st = run_prune(fa)) != QVG_OK) return fail(st);
             // 3. reverse edges grouped by target
             const uint32_t np = nb * R;
@@ -722,7 +758,7 @@ extern "C" qvg_status qvg_robust_prune(qvg_index* h, uint64_t ntasks, const uint
             return QVG_INVALID_ARGUMENT;
         }
         if (off[t + 1] - off[t] > kMaxCand) {
-            set_error("qvg_robust_prune: more than 256 candidates in one task");
+            set_error("qvg_robust_prune: more than 480 candidates in one task");
             return QVG_NOT_IMPLEMENTED;
         }
     }

@@ -138,6 +138,11 @@ struct SearchLaunch {
     uint32_t* tie_spill;
     uint32_t tie_spill_cap;
     const uint32_t* qmap;
+    // builder searches (non-LEAN kernels): keys (dist<<33 | id) of the first
+    // exp_cap expanded nodes of query q at exp_out[q * exp_cap ...], count exp_n[q]
+    uint64_t* exp_out;
+    uint32_t* exp_n;
+    uint32_t exp_cap;
 };
 
 // keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)

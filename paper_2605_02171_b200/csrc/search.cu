@@ -926,7 +926,13 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 u = tie[tn - 1];
                 --tn;
                 ++c_tie;
+                spec_key = mkkey(tdist, u);  // (the expanded-node list below)
             }
+            // builder searches: the expanded nodes in expansion order — Vamana's
+            // visited set V, the RobustPrune candidates of the build's second
+            // pass (never in LEAN kernels)
+            if (!LEAN && !REL && a.exp_out && lane == 0 && c_exp < a.exp_cap)
+                a.exp_out[q * a.exp_cap + c_exp] = ordk(spec_key);
             if (!REL) ++c_exp;
 
             // (g) adjacency row (stored order): the speculative prefetch when it
@@ -1005,6 +1011,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             }
             if (lane == 0) a.pool_n[q] = np;
         }
+        if (!LEAN && a.exp_out && lane == 0) a.exp_n[q] = min(c_exp, a.exp_cap);
         const int32_t qstatus = overflow ? QVG_Q_TIE_OVERFLOW : QVG_Q_OK;
         if (lane == 0 && overflow && a.flags) atomicOr(a.flags, 1u << QVG_Q_TIE_OVERFLOW);
         if (lane == 0) {
@@ -1195,7 +1202,7 @@ bool geo_allowed(const SearchLaunch& a) {
         const char* e = getenv("QVG_LEAN");
         return !(e && e[0] == '0');
     }();
-    return env_ok && !a.exact_bits && !(a.variant & 8u) && !a.tie_spill && !a.qmap;
+    return env_ok && !a.exact_bits && !(a.variant & 8u) && !a.tie_spill && !a.qmap && !a.exp_out;
 }
 
 uint32_t pow2ceil(uint32_t x) {

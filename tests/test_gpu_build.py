@@ -108,7 +108,7 @@ def test_gpu_robust_prune_equals_reference_function(R):
     with qivr::robust_prune (graph.hpp:162-183) on identical candidate lists:
     heavy distance ties (tiny-D codes: pairwise SM2 distances take a handful of
     values; candidate dists drawn from a small range or equal to the true
-    distance to a target), alpha in {1.0, 1.2}, up to 256 candidates."""
+    distance to a target), alpha in {1.0, 1.2}, up to 480 candidates."""
     rng = np.random.Generator(np.random.PCG64(R))
     for dim, n in ((8, 3000), (64, 3000), (768, 1500)):
         base = rng.standard_normal((n, dim)).astype(np.float32)
@@ -117,7 +117,7 @@ def test_gpu_robust_prune_equals_reference_function(R):
         codes = ref.codes()
         tasks = []
         for t in range(120):
-            nc = int(rng.integers(1, 257))
+            nc = int(rng.integers(1, 481 if n > 480 else n))
             ids = rng.choice(n, nc, replace=False).astype(np.uint32)
             if t % 3 == 0:  # dists = true BQ distance to a target (as link_node)
                 tgt = int(rng.integers(0, n))
@@ -143,7 +143,7 @@ def test_gpu_robust_prune_validates_like_a_boundary():
     with pytest.raises(Q.InvalidArgument):
         ix.robust_prune([(np.array([100], np.uint32), np.array([1], np.uint32))], 8, 1.2)
     with pytest.raises(Q.NotImplementedByQvg):
-        ix.robust_prune([(np.arange(100, dtype=np.uint32).repeat(3)[:257],
-                          np.zeros(257, np.uint32))], 8, 1.2)
+        ix.robust_prune([(np.arange(100, dtype=np.uint32).repeat(5)[:481],
+                          np.zeros(481, np.uint32))], 8, 1.2)
     assert [a.tolist() for a in ix.robust_prune([(np.empty(0, np.uint32),
                                                   np.empty(0, np.uint32))], 8, 1.2)] == [[]]
