@@ -145,6 +145,21 @@ struct SearchLaunch {
     uint32_t exp_cap;
 };
 
+// Visited-table entry width (bytes) for n nodes and 2^lg slots.  The table
+// hashes id by a bijection on b = bits(n - 1) bits (id * odd mod 2^b): the top
+// lg bits pick the slot, the low b - lg bits are the tag, so a tag of <= 7 /
+// <= 15 bits fits a byte / a short and slot + tag still identify the id
+// exactly (no false "visited"); wider tags keep full 32-bit ids.
+__host__ __device__ inline uint32_t vis_id_bits(uint64_t n) {
+    uint32_t b = 1;
+    while (b < 32 && (1ull << b) < n) ++b;
+    return b;
+}
+__host__ __device__ inline uint32_t vis_tag_bytes(uint64_t n, uint32_t lg) {
+    const int tb = (int)vis_id_bits(n) - (int)lg;
+    return tb <= 7 ? 1u : (tb <= 15 ? 2u : 4u);
+}
+
 // keys kept beyond the pool for a rerank deeper than ef (0 = reference depth)
 __host__ __device__ inline uint32_t extra_depth(uint32_t ef, uint32_t depth) { return depth > ef ? depth - ef : 0u; }
 

@@ -111,7 +111,7 @@ struct SmemLayout {
 // EFM = pool + extra-depth capacity rounded to 32; xa > 0 adds the extra-depth
 // candidate buffers.
 __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uint32_t W,
-                                                  uint32_t tie_cap, uint32_t vis_slots,
+                                                  uint32_t tie_cap, uint32_t vis_bytes,
                                                   uint32_t stage_rows, uint32_t xa = 0,
                                                   bool lean_ranks = false, bool geo = false) {
     SmemLayout L;
@@ -140,7 +140,10 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.stg = L.crp;               // tie-stack additions (crp is dead by then)
     L.qc = take(16 * W, 16);     // query code chunks
     L.tie = take(4 * tie_cap, 16);
-    L.vis = take(4 * vis_slots, 16);  // rerank scores alias this region (vis_slots >= EFM)
+    // visited table (vis_bytes = slots x entry width); the rerank scores
+    // (EFM floats) alias this region
+    // (geo: full-id slots, and plan_search keeps slots >= EFM)
+    L.vis = take(geo || vis_bytes > 4 * EFM ? vis_bytes : 4 * EFM, 16);
     L.qsl = geo && 8 * RM >= 2 * 48 * 4 ? L.ctd : take(2 * 48 * 4, 16);  // rerank query slices
     // extra depth: A candidates of one step (<= RM: each scored key is a P
     // contender or an A candidate, and evictions <= P contenders), sorted copy
@@ -229,7 +232,14 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     const uint32_t ef = a.ef;  // (a compile-time ef = 64 instantiation measured +0.3 %)
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS, SR, xa, true, GEO);
+    // visited-table entry width: byte / short tags where they identify ids
+    // exactly, else full ids (the headline geometry keeps full ids: its table
+    // is small and its lossy re-evaluations are ~2 %)
+    const uint32_t vtw = GEO ? 4u : vis_tag_bytes(ix.n, a.vis_log2);
+    const uint32_t vbits = GEO ? 32u : vis_id_bits(ix.n);
+    const uint32_t vmask = vbits >= 32 ? ~0u : (1u << vbits) - 1u;
+    const uint32_t vtb = vbits > a.vis_log2 ? vbits - a.vis_log2 : 0u;  // tag bits
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, GEO ? 4u * VS : VS * vtw, SR, xa, true, GEO);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -254,6 +264,29 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
     float* qsl = reinterpret_cast<float*>(base + L.qsl);
+    // visited-table test-and-set: true if `id` was not recorded (lossy: a
+    // forgotten node is only re-scored, never wrongly skipped)
+    auto vis_insert = [&](uint32_t id) -> bool {
+        if constexpr (GEO) return true;  // (never called: GEO inlines the full-id table)
+        if (vtw == 4u) {
+            const uint32_t s = vhash(id, a.vis_log2);
+            if (vis[s] == id) return false;
+            vis[s] = id;
+            return true;
+        }
+        const uint32_t mx = (id * 0x9E3779B1u) & vmask;
+        const uint32_t s = mx >> vtb, tg = mx & ((1u << vtb) - 1u);
+        if (vtw == 1u) {
+            uint8_t* v8 = reinterpret_cast<uint8_t*>(vis);
+            if (v8[s] == tg) return false;
+            v8[s] = (uint8_t)tg;
+            return true;
+        }
+        uint16_t* v16 = reinterpret_cast<uint16_t*>(vis);
+        if (v16[s] == tg) return false;
+        v16[s] = (uint16_t)tg;
+        return true;
+    };
     uint64_t* acd = reinterpret_cast<uint64_t*>(base + L.acd);
     uint64_t* axk = reinterpret_cast<uint64_t*>(base + L.axk);
     uint32_t* axr = reinterpret_cast<uint32_t*>(base + L.axr);
@@ -441,12 +474,14 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             for (uint64_t i = lane; i < a.exact_words / 4; i += 32) xb4[i] = make_uint4(0, 0, 0, 0);
             __syncwarp();
         } else {
-            for (uint32_t i = lane; i < VS; i += 32) vis[i] = kSentinel;
+            const uint32_t vwords = GEO ? VS : (VS * vtw) / 4u;
+            for (uint32_t i = lane; i < vwords; i += 32) vis[i] = kSentinel;  // all 0xFF
         }
         const uint32_t entry = a.entry;
         if (lane == 0) {
             if (xbits) atomicOr(xbits + (entry >> 5), 1u << (entry & 31));
-            else vis[vhash(entry, a.vis_log2)] = entry;
+            else if (GEO) vis[vhash(entry, a.vis_log2)] = entry;
+            else vis_insert(entry);
         }
         uint32_t np = 0, tn = 0, tdist = 0, hint = 0;
         uint32_t na = 0;  // |A| (XA only)
@@ -926,7 +961,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 u = tie[tn - 1];
                 --tn;
                 ++c_tie;
-                spec_key = mkkey(tdist, u);  // (the expanded-node list below)
+                if (!LEAN && a.exp_out) spec_key = mkkey(tdist, u);  // (expanded-node list)
             }
             // builder searches: the expanded nodes in expansion order — Vamana's
             // visited set V, the RobustPrune candidates of the build's second
@@ -976,9 +1011,13 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                         const uint32_t bit = 1u << (id & 31);
                         k2 = (atomicOr(xbits + (id >> 5), bit) & bit) == 0;
                     } else {
-                        const uint32_t s = vhash(id, a.vis_log2);
-                        if (vis[s] == id) k2 = false;
-                        else vis[s] = id;
+                        if constexpr (GEO) {  // full ids (codegen of the headline kernel kept)
+                            const uint32_t s = vhash(id, a.vis_log2);
+                            if (vis[s] == id) k2 = false;
+                            else vis[s] = id;
+                        } else {
+                            k2 = vis_insert(id);
+                        }
                     }
                 }
                 keep[j] = k2;
@@ -1311,7 +1350,8 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
-                                     1u << vis_log2, p.SR, xa, true, p.geo);
+                                     (1u << vis_log2) * (p.geo ? 4u : vis_tag_bytes(ix.n, vis_log2)),
+                                     p.SR, xa, true, p.geo);
     p.warp_bytes = L.total;
     if (p.geo || p.one) {
         // one block per SM with as many warps as its shared memory holds (the
@@ -1403,7 +1443,7 @@ uint32_t auto_visited_log2(const DevIndex& ix, uint32_t ef, uint32_t tie_cap, in
     while ((1u << min_log) < ((ef + xa + 31u) & ~31u)) ++min_log;  // rerank scores alias it
     uint32_t best_log = min_log;
     int best_blocks = -1;
-    for (uint32_t lg = min_log; lg <= 12 || lg == min_log; ++lg) {
+    for (uint32_t lg = min_log; lg <= 15 || lg == min_log; ++lg) {
         const Plan p = make_plan(ix, ef, lg, tie_cap, xa, relax);
         if (p.block_bytes > max_dyn_smem(device) || !allow_max_smem(p.fn, device)) {
             break;

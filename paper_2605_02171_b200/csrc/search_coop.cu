@@ -54,6 +54,8 @@ __device__ __forceinline__ void coop_ev(uint64_t q, uint32_t iter_q, int ev) {
 #define QVG_CP(...)
 #endif
 
+__host__ __device__ inline uint32_t coop_vis_log2(uint32_t lg) { return lg < 12u ? lg : 12u; }
+
 struct CoopLayout {
     uint32_t bars, stages, stage_bytes, pk, ctd, evk, crp, csrp, cid, stg, dsh, spec, smin, scop, hctd,
         hcrp, hcnt, hdrop, qc, tie, vis, qn, ctl, total;
@@ -114,7 +116,10 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
     const uint32_t W = ix.W;
     const uint32_t rowb = 16u * W;
     const uint32_t gstride = group_stride(W);
-    const uint32_t VS = 1u << a.vis_log2;
+    // the block's own visited table: full ids, at most 4096 slots (the
+    // per-warp kernel's table size may be chosen for byte tags)
+    const uint32_t vlg = coop_vis_log2(a.vis_log2);
+    const uint32_t VS = 1u << vlg;
     const uint32_t ef = a.ef;
     const uint32_t EFM = (ef + 31u) & ~31u;
     const CoopLayout L = coop_layout(EFM, RM, W, a.tie_cap, VS, ix.Dp, SRW);
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
         const uint32_t entry = a.entry;
         __syncthreads();
         if (tid == 0) {
-            vis[vhash(entry, a.vis_log2)] = entry;
+            vis[vhash(entry, vlg)] = entry;
             cid[0] = entry;
             *ctl_n = 1;
             *ctl_done = 0;
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                         const uint32_t id = v[j];
                         bool k2 = id != kSentinel;
                         if (k2) {
-                            const uint32_t sidx = vhash(id, a.vis_log2);
+                            const uint32_t sidx = vhash(id, vlg);
                             if (vis[sidx] == id) k2 = false;
                             else vis[sidx] = id;
                         }
@@ -710,7 +715,8 @@ CoopPlan coop_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t 
     // rows per helper warp (the leader scores none): a multiple of 4
     p.SRW = (((RM + kCoopWarps - 2) / (kCoopWarps - 1)) + 3u) & ~3u;
     p.block_bytes =
-        coop_layout((ef + 31) & ~31u, RM, ix.W, tie_cap, 1u << vis_log2, ix.Dp, p.SRW).total;
+        coop_layout((ef + 31) & ~31u, RM, ix.W, tie_cap, 1u << coop_vis_log2(vis_log2), ix.Dp,
+                    p.SRW).total;
     return p;
 }
 
