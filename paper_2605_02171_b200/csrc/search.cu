@@ -807,13 +807,25 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 const uint32_t lo = mu ? csrp[0] : np;
                 ins_lo = lo;
                 const uint32_t total = np + mu;
+                // few contenders (the usual case): their ranks padded to 8 with
+                // +inf, two broadcast 16-B loads per chunk and eight compares
+                // instead of a dependent binary search per pool entry
+                const bool few = mu <= 8u;
+                if (few && lane >= mu && lane < 8u) csrp[lane] = 0xFFFFFFFFu;
+                __syncwarp();
                 if (lo < np) {
                     for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
                         const uint32_t idx = (uint32_t)cb + lane;
                         const bool mv = idx < np && idx >= lo;
                         uint64_t p = 0;
                         uint32_t npos = 0;
-                        if (mv) {
+                        if (few) {
+                            const uint4 r0 = reinterpret_cast<const uint4*>(csrp)[0];
+                            const uint4 r1 = reinterpret_cast<const uint4*>(csrp)[1];
+                            if (mv) p = pk[idx];
+                            npos = idx + (r0.x <= idx) + (r0.y <= idx) + (r0.z <= idx) + (r0.w <= idx) +
+                                   (r1.x <= idx) + (r1.y <= idx) + (r1.z <= idx) + (r1.w <= idx);
+                        } else if (mv) {
                             p = pk[idx];
                             npos = idx + upper_bound_u32(csrp, mu, idx);
                         }

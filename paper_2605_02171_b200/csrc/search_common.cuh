@@ -48,36 +48,39 @@ __device__ __forceinline__ void tma_gather4_col(void* dst, const CUtensorMap* ma
     dev::tma_gather4(dst, map, col, r0, r1, r2, r3, bar);
 }
 
-// Row distance accumulator in bit planes (Harley-Seal carry-save adders).
-// Per chunk the SM2 terms are four weight-1 words (x0, x1, o0, o1) and two
-// weight-2 words (a0, a1) (encoding.hpp:169-176: popc(x) + popc(x & (sa|sb)) +
-// 2 popc(x & sa & sb)).  Adding them through CSAs (LOP3s on the ALU pipe)
-// leaves one POPC per chunk instead of six: POPC runs on the XU pipe at a
-// quarter of the ALU rate on B200 (tools/popc_bench.cu: 0.5 vs 2 warp-ops per
-// SM per cycle), and the XU pipe was the busiest in the search kernel.
+// Row distance accumulator in bit planes (carry-save adders).  Per chunk the
+// SM2 terms are four weight-1 words (x0, x1, o0, o1) and two weight-2 words
+// (a0, a1) (encoding.hpp:169-176: popc(x) + popc(x & (sa|sb)) +
+// 2 popc(x & sa & sb)).  LOP3 runs on the ALU pipe (2 warp-ops per SM per
+// cycle) and POPC on the XU pipe (0.5; tools/popc_bench.cu), and the distance
+// loop is ALU-pipe bound (ncu: math-pipe throttle on the CSA lines), so the
+// reduction stops where the two pipes balance: three CSAs fold the four
+// weight-1 words and their two carries, and the three words left per chunk
+// (one weight-4 carry, a0, a1) are counted at once.  14 ALU + 3 XU ops per
+// chunk; measured on cfg 2 (same box, profiles/r2e_sm2acc_ab.txt): six POPCs
+// (round 1 start) XU bound; five CSAs + a weight-8 half adder, 19 ALU + 1 XU
+// (round 1 final) 4.17 M QPS; four CSAs 4.37 M; three CSAs (this) 4.39 M;
+// two CSAs 4.36 M.
 __device__ __forceinline__ void csa(uint32_t& a, uint32_t b, uint32_t c, uint32_t& carry) {
     const uint32_t u = a ^ b;
     carry = (a & b) | (u & c);
     a = u ^ c;
 }
 struct Sm2Acc {
-    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, d16 = 0;
+    uint32_t ones = 0, twos = 0, d2 = 0, d4 = 0;
     __device__ __forceinline__ void add(const uint4 q, const uint4 v) {
         const uint32_t x0 = q.x ^ v.x, x1 = q.y ^ v.y;
         const uint32_t o0 = x0 & (q.z | v.z), o1 = x1 & (q.w | v.w);
         const uint32_t a0 = x0 & q.z & v.z, a1 = x1 & q.w & v.w;
-        uint32_t c1, c2, f1, f2, e;
-        csa(ones, x0, x1, c1);   // weight 1 -> carries of weight 2
+        uint32_t c1, c2, f1;
+        csa(ones, x0, x1, c1);  // weight 1 -> carries of weight 2
         csa(ones, o0, o1, c2);
-        csa(twos, c1, c2, f1);   // weight 2 -> carries of weight 4
-        csa(twos, a0, a1, f2);
-        csa(fours, f1, f2, e);   // weight 4 -> carry of weight 8
-        d16 += __popc(eights & e);  // half adder at weight 8, carry counted
-        eights ^= e;
+        csa(twos, c1, c2, f1);  // weight 2 -> carry of weight 4
+        d4 += __popc(f1);  // (IMAD adds, to move them to the FMA pipe: no gain)
+        d2 += __popc(a0) + __popc(a1);
     }
     __device__ __forceinline__ uint32_t total() const {
-        return __popc(ones) + 2u * __popc(twos) + 4u * __popc(fours) + 8u * __popc(eights) +
-               16u * d16;
+        return __popc(ones) + 2u * (__popc(twos) + d2) + 4u * d4;
     }
 };
 
@@ -115,15 +118,24 @@ __device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
     return acc.total();
 }
 
-// first index i in [0, n) with ordk(a[i]) >= x
+// first index i in [0, n) with ordk(a[i]) >= x.  4-ary: three independent
+// pivot loads per round, half the dependent shared-memory round trips of a
+// binary search (cfg 2 ef 256: 10.16 -> 10.13 ms; with the merge's broadcast
+// shift 9.79 ms, profiles/r2e_sm2acc_ab.txt)
 __device__ __forceinline__ uint32_t lower_bound_key(const uint64_t* a, uint32_t n, uint64_t x) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (ordk(a[mid]) < x) lo = mid + 1;
-        else hi = mid;
+    uint32_t lo = 0;
+    while (n >= 4) {
+        const uint32_t q = n >> 2;
+        const uint64_t k1 = ordk(a[lo + q - 1]), k2 = ordk(a[lo + 2 * q - 1]),
+                       k3 = ordk(a[lo + 3 * q - 1]);
+        const uint32_t c = (uint32_t)(k1 < x) + (uint32_t)(k2 < x) + (uint32_t)(k3 < x);
+        lo += c * q;
+        n = c == 3 ? n - 3 * q : q - 1;
     }
-    return lo;
+    uint32_t r = 0;
+#pragma unroll
+    for (uint32_t i = 0; i < 3; ++i) r += (i < n && ordk(a[lo + i]) < x) ? 1u : 0u;
+    return lo + r;
 }
 
 // #{j < m : a[j] <= x} for non-decreasing a
