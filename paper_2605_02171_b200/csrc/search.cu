@@ -129,9 +129,14 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.stage1 = take((stage_rows / 4) * group_stride(W), 128);
     if (geo) L.bars = take(16, 16);
     L.pk = take(8 * EFM, 16);    // pool keys P[0, ef), then extra-depth keys A
-    L.ctd = take(8 * RM, 16);    // contenders, row order
+    // contenders (row order) and their ranks in P.  geo: in stage half 0 — an
+    // expansion has at most two halves there, every lane has consumed half 0
+    // before the first contender is stored (the ballot in emit), and the
+    // buffers are dead before the next step's TMA refills it (the proxy fence
+    // in issue() orders these generic writes before the TMA's)
+    L.ctd = geo ? L.stage0 : take(8 * RM, 16);
     L.evk = L.ctd;               // keys evicted this step (ctd is dead by then)
-    L.crp = take(4 * RM, 16);    // contender rank in P, row order
+    L.crp = geo ? L.stage0 + 8 * RM : take(4 * RM, 16);  // contender rank in P, row order
     // contender rank in P, key order (lean_ranks: in the compacted-id buffer,
     // which is dead between the last distance pass and the next compaction)
     L.csrp = lean_ranks ? 0 : take(4 * RM, 16);
@@ -144,7 +149,9 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     // (EFM floats) alias this region
     // (geo: full-id slots, and plan_search keeps slots >= EFM)
     L.vis = take(geo || vis_bytes > 4 * EFM ? vis_bytes : 4 * EFM, 16);
-    L.qsl = geo && 8 * RM >= 2 * 48 * 4 ? L.ctd : take(2 * 48 * 4, 16);  // rerank query slices
+    // rerank query slices (geo: over the compacted-id buffer and the query
+    // code, contiguous and both dead during the rerank)
+    L.qsl = geo && 4 * RM + 16 * W >= 2 * 48 * 4 ? L.cid : take(2 * 48 * 4, 16);
     // extra depth: A candidates of one step (<= RM: each scored key is a P
     // contender or an A candidate, and evictions <= P contenders), sorted copy
     // and their ranks in A
@@ -222,7 +229,9 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     constexpr int SPL = REL ? RW / RELP : RW;  // adjacency slots per lane per picked row
     static_assert(!REL || (SPL >= 1 && SPL * RELP == RW && !XA), "relaxed geometry");
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t wib = threadIdx.x >> 5;
+    // (broadcast from lane 0: tells the compiler the warp index, and every
+    // shared-memory address derived from it, is warp-uniform; cfg 2 +0.5 %)
+    const uint32_t wib = __shfl_sync(0xFFFFFFFFu, threadIdx.x >> 5, 0);
     const uint32_t lt_mask = (1u << lane) - 1u;
     const DevIndex ix = a.ix;
     const uint32_t W = WC ? (uint32_t)WC : ix.W;
@@ -311,12 +320,17 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     uint32_t phs = 0;  // bit h = phase parity of bars[h]
 
     // issue the TMA fetch of compacted rows [r0, r0+cnt) into stage half h
-    auto issue = [&](uint32_t r0, uint32_t cnt, uint32_t h) {
+    auto issue = [&](uint32_t r0, uint32_t cnt, uint32_t h, bool fence = true) {
         uint64_t* bar = &bars[h];
         const uint32_t ng = use_tmap ? (cnt + 3u) >> 2 : cnt;
         const uint32_t bytes = use_tmap ? ng * 4u * rowb : cnt * rowb;
-        TMA_WAR_FENCE();  // order this lane's reads of the half before TMA writes
-        __syncwarp();         // all lanes finished reading this half
+        if (fence) {
+            TMA_WAR_FENCE();  // order this lane's reads of the half before TMA writes
+            __syncwarp();         // all lanes finished reading this half
+        }
+        // (one elected lane issuing every group in a warp-uniform loop, with
+        // broadcast index loads, measured 12 % slower than this per-lane
+        // election loop: profiles/r2f_issue_ab.txt)
         if (lane == 0) mbar_expect_tx(bar, bytes);
         __syncwarp();
         for (uint32_t g = lane; g < ng; g += 32) {
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             // (a) TMA-gather the code rows (double-buffered halves of SR rows)
             const uint32_t nsub = __umulhi(n + SR - 1, sr_m);  // (n + SR - 1) / SR
             if (nsub > 0) issue(0, min(n, SR), 0);
-            if (nsub > 1) issue(SR, min(n - SR, SR), 1);
+            if (nsub > 1) issue(SR, min(n - SR, SR), 1, false);  // (same fence covers both halves)
             QVG_PH(ph_tma += clock64() - tp0;)
             // speculative prefetch: adjacency row of the current best unexpanded
             // entry (the next pick unless this row inserts a better one)
