@@ -105,13 +105,26 @@ struct Out {
     bool copy_back = false;
 };
 
-qvg_status bind_out(Out& o, void* user, Buffer& scratch, size_t bytes, bool needed) {
+// `mapped_ok`: a pinned host buffer is written by the kernel itself through
+// its device alias (posted PCIe writes as each query finishes) instead of a
+// device scratch buffer plus a D2H copy after the launch — only for the small
+// per-query results (k ids / scores, count, status)
+qvg_status bind_out(Out& o, void* user, Buffer& scratch, size_t bytes, bool needed,
+                    bool mapped_ok = false) {
     o.user = user;
     o.bytes = bytes;
     if (!user && !needed) return QVG_OK;
-    if (user && is_device_ptr(user)) {
-        o.dev = user;
-        return QVG_OK;
+    if (user) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, user) != cudaSuccess) {
+            cudaGetLastError();
+        } else if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+            o.dev = user;
+            return QVG_OK;
+        } else if (mapped_ok && at.type == cudaMemoryTypeHost && at.devicePointer) {
+            o.dev = at.devicePointer;
+            return QVG_OK;
+        }
     }
     qvg_status st = grow(scratch, bytes);
     if (st != QVG_OK) return st;
@@ -251,10 +264,14 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     if ((st = grow(h->s_counter, 64)) != QVG_OK) return st;
     if (!in_dev && (st = grow(h->s_in, in_bytes)) != QVG_OK) return st;
     Out o_ids, o_sc, o_cnt, o_st, o_pi, o_pd, o_pn, o_ctr;
-    if ((st = bind_out(o_ids, out_ids, h->s_ids, nq * k * 4ull, do_rerank)) != QVG_OK) return st;
-    if ((st = bind_out(o_sc, out_scores, h->s_sc, nq * k * 4ull, do_rerank)) != QVG_OK) return st;
-    if ((st = bind_out(o_cnt, out_count, h->s_cnt, nq * 4ull, do_rerank)) != QVG_OK) return st;
-    if ((st = bind_out(o_st, out_query_status, h->s_st, nq * 4ull, true)) != QVG_OK) return st;
+    static const bool zc = [] {  // QVG_ZEROCOPY=0: always stage results in HBM (A/B)
+        const char* v = getenv("QVG_ZEROCOPY");
+        return !(v && v[0] == '0');
+    }();
+    if ((st = bind_out(o_ids, out_ids, h->s_ids, nq * k * 4ull, do_rerank, zc)) != QVG_OK) return st;
+    if ((st = bind_out(o_sc, out_scores, h->s_sc, nq * k * 4ull, do_rerank, zc)) != QVG_OK) return st;
+    if ((st = bind_out(o_cnt, out_count, h->s_cnt, nq * 4ull, do_rerank, zc)) != QVG_OK) return st;
+    if ((st = bind_out(o_st, out_query_status, h->s_st, nq * 4ull, true, zc)) != QVG_OK) return st;
     if ((st = bind_out(o_pi, out_pool_ids, h->s_pool_i, nq * ef * 4ull, false)) != QVG_OK) return st;
     if ((st = bind_out(o_pd, out_pool_dists, h->s_pool_d, nq * ef * 4ull, o_pi.dev != nullptr)) != QVG_OK) return st;
     if ((st = bind_out(o_pn, out_pool_size, h->s_pool_n, nq * 4ull, o_pi.dev != nullptr)) != QVG_OK) return st;
@@ -344,6 +361,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         const long long c = v ? atoll(v) : 1024;
         return (uint64_t)(c < 32 ? 32 : c);
     }();
+    bool launched = false;
     const bool stage_ok = 4ull * ix.dim <= search_stage_bytes(ix);
     const bool pipelined = mode.encode && !in_dev && pipe_env && stage_ok && nq >= 2 * kChunk;
     cudaEventRecord(h->ev[0], s);
@@ -356,7 +374,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     cudaMemsetAsync(h->s_counter.p, 0, 64, s);  // work counter + flag word + ready count
     cudaEventRecord(h->ev[1], s);
     const bool fused = mode.encode && stage_ok && (fused_env || pipelined);
-    if (pipelined && (st = ensure_copy_stream(h, (nq + kChunk - 1) / kChunk)) != QVG_OK) return st;
+    if (pipelined && (st = ensure_copy_stream(h, (nq + kChunk - 1) / kChunk + 5)) != QVG_OK) return st;
     if (fused) {
         // K1 runs as the search kernel's per-query prologue
         a.qraw = static_cast<const float*>(din);
@@ -394,39 +412,48 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     // each cudaMemcpyAsync, so its chunks are submitted after the launch (the
     // kernel runs while the driver stages them); under such tools use
     // QVG_PIPELINE=0 for pageable host queries.
+    // (a ramped schedule — 128 / 256 / 512-query first chunks, only the first
+    // submitted before the launch — measured 0.4 % slower end to end than
+    // uniform chunks submitted first: profiles/r2k_e2e_ab.txt)
     const bool copies_first = pipelined && (is_pinned_host_ptr(user_in) || under_tool());
-    auto submit_chunks = [&]() -> qvg_status {
+    uint64_t next_c0 = 0, next_c = 0;
+    bool chunks_started = false;
+    auto submit_chunks = [&](uint64_t max_chunks) -> qvg_status {
         // Each chunk's ready count is a 4-byte copy ordered after its rows on
         // the copy stream; the chunks start after the counter reset (ev[1]).
         cudaStream_t cs = h->copy_stream;
-        cudaStreamWaitEvent(cs, h->ev[1], 0);
+        if (!chunks_started) cudaStreamWaitEvent(cs, h->ev[1], 0);
+        chunks_started = true;
         const size_t row = (size_t)ix.dim * 4;
-        for (uint64_t c0 = 0, c = 0; c0 < nq; c0 += kChunk, ++c) {
-            const uint64_t c1 = c0 + kChunk < nq ? c0 + kChunk : nq;
+        for (uint64_t done = 0; next_c0 < nq && done < max_chunks; ++done, ++next_c) {
+            const uint64_t c0 = next_c0;
+            const uint64_t len = kChunk;
+            const uint64_t c1 = c0 + len < nq ? c0 + len : nq;
+            next_c0 = c1;
             e = cudaMemcpyAsync(static_cast<char*>(h->s_in.p) + c0 * row,
                                 static_cast<const char*>(user_in) + c0 * row, (c1 - c0) * row,
                                 cudaMemcpyHostToDevice, cs);
             if (e == cudaSuccess) {
-                h->ready_host[c] = (uint32_t)c1;
-                e = cudaMemcpyAsync(d_ready, &h->ready_host[c], 4, cudaMemcpyHostToDevice, cs);
+                h->ready_host[next_c] = (uint32_t)c1;
+                e = cudaMemcpyAsync(d_ready, &h->ready_host[next_c], 4, cudaMemcpyHostToDevice, cs);
             }
             if (e != cudaSuccess) {
                 // never leave a running kernel waiting: release every query
                 // (a copy-engine write; no SM is free while the search runs)
-                if (!copies_first) {
-                    const uint64_t last = (nq + kChunk - 1) / kChunk - 1;
-                    h->ready_host[last] = (uint32_t)nq;
-                    cudaMemcpyAsync(d_ready, &h->ready_host[last], 4, cudaMemcpyHostToDevice, cs);
+                if (launched) {
+                    h->ready_host[next_c + 1] = (uint32_t)nq;
+                    cudaMemcpyAsync(d_ready, &h->ready_host[next_c + 1], 4, cudaMemcpyHostToDevice, cs);
                 }
                 cudaStreamSynchronize(cs);
-                if (!copies_first) cudaStreamSynchronize(s);
+                if (launched) cudaStreamSynchronize(s);
                 return cuda_status(e, "H2D(queries, pipelined)");
             }
         }
-        cudaEventRecord(h->ev_copy, cs);
+        if (next_c0 >= nq) cudaEventRecord(h->ev_copy, cs);
         return QVG_OK;
     };
-    if (copies_first && (st = submit_chunks()) != QVG_OK) return st;
+    const uint64_t kAll = ~0ull;
+    if (copies_first && (st = submit_chunks(kAll)) != QVG_OK) return st;
     if (coop) {
         st = launch_coop(a, &h->tmap, s, h->device, &grid);
         pinfo.warps_per_block = kCoopWarps;  // reported in stats: the latency kernel ran
@@ -434,10 +461,11 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         st = launch_search(a, h->has_tmap ? &h->tmap : nullptr, grid, s);
     }
     if (st != QVG_OK) {
-        if (copies_first) cudaStreamSynchronize(h->copy_stream);  // no copy outlives the call
+        if (chunks_started) cudaStreamSynchronize(h->copy_stream);  // no copy outlives the call
         return st;
     }
-    if (pipelined && !copies_first && (st = submit_chunks()) != QVG_OK) return st;
+    launched = true;
+    if (pipelined && !copies_first && (st = submit_chunks(kAll)) != QVG_OK) return st;
     if (pipelined) cudaStreamWaitEvent(s, h->ev_copy, 0);  // results after every chunk
     cudaEventRecord(h->ev[3], s);
     Out* outs[] = {&o_ids, &o_sc, &o_cnt, &o_st, &o_pi, &o_pd, &o_pn, &o_ctr};
@@ -479,7 +507,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     uint64_t n_spilled = 0;
     if (hflags & (1u << QVG_Q_TIE_OVERFLOW)) {
         std::vector<int32_t> qs(nq);
-        e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost);
+        e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDefault);  // (HBM or mapped host)
         if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
         std::vector<uint32_t> redo;
         for (uint64_t i = 0; i < nq; ++i)
@@ -589,7 +617,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     // rare path: locate the first offending query (the reference's
     // single-threaded batch throws at the first invalid one)
     std::vector<int32_t> qs(nq);
-    e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(qs.data(), o_st.dev, nq * 4, cudaMemcpyDefault);
     if (e != cudaSuccess) return cuda_status(e, "D2H(status)");
     int64_t first_bad = -1, first_ovf = -1;
     for (uint64_t i = 0; i < nq; ++i) {
