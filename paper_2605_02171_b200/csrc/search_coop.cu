@@ -340,6 +340,24 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                 uint32_t ins_lo = kSentinel;
                 if (pend_m > 0) {
                     const uint32_t m = pend_m;
+                    {  // the helpers' contenders of the last expansion, in row order
+                        uint32_t off[kCoopWarps - 1];
+                        uint32_t mm = 0;
+#pragma unroll
+                        for (int hh = 0; hh < kCoopWarps - 1; ++hh) {
+                            off[hh] = mm;
+                            mm += hcnt[hh];
+                        }
+                        for (uint32_t i = lane; i < m; i += 32) {
+                            uint32_t k2 = i;  // slot in the helper segments (constant indices
+#pragma unroll                                // only: a runtime index would spill off[])
+                            for (int t = 1; t < kCoopWarps - 1; ++t)
+                                if (i >= off[t]) k2 = t * SRW + (i - off[t]);
+                            ctd[i] = hctd[k2];
+                            crp[i] = hcrp[k2];
+                        }
+                        __syncwarp();
+                    }
                     // (c) contender ranks (key order) and prefix counts (row order)
                     uint64_t y[RW];
                     uint32_t rk[RW], pre[RW], rpv[RW];
@@ -499,13 +517,11 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
             if (w == 0) {
                 // ---- phase B (leader): the helpers' contenders in row order
                 c_eval += n;
-                uint32_t off[kCoopWarps - 1];
                 uint32_t m = 0;
                 uint64_t kmin = kInfKey;
                 int hsrc = -1;
 #pragma unroll
                 for (int hh = 0; hh < kCoopWarps - 1; ++hh) {
-                    off[hh] = m;
                     m += hcnt[hh];
                     const uint64_t km = smin[hh];
                     if (km < kmin) {
@@ -513,15 +529,9 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                         hsrc = hh;
                     }
                 }
-                for (uint32_t i = lane; i < m; i += 32) {
-                    uint32_t k2 = i;  // slot in the helper segments (constant indices only:
-#pragma unroll                        // a runtime index would put off[] in local memory)
-                    for (int t = 1; t < kCoopWarps - 1; ++t)
-                        if (i >= off[t]) k2 = t * SRW + (i - off[t]);
-                    ctd[i] = hctd[k2];
-                    crp[i] = hcrp[k2];
-                }
-                __syncwarp();
+                // (the slices are concatenated into ctd / crp at the start of
+                // the next phase C, off the critical path: the helpers rewrite
+                // them only after that phase's barrier)
                 QVG_CP(coop_ev(q, it_q, 3);)
                 // (f) pick: the smallest contender is always admitted, so the
                 // best unexpanded entry of P' is min(predicted pick, kmin); with
