@@ -147,8 +147,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.tie = take(4 * tie_cap, 16);
     // visited table (vis_bytes = slots x entry width); the rerank scores
     // (EFM floats) alias this region
-    // (geo: full-id slots, and plan_search keeps slots >= EFM)
-    L.vis = take(geo || vis_bytes > 4 * EFM ? vis_bytes : 4 * EFM, 16);
+    L.vis = take(vis_bytes > 4 * EFM ? vis_bytes : 4 * EFM, 16);
     // rerank query slices (geo: over the compacted-id buffer and the query
     // code, contiguous and both dead during the rerank)
     L.qsl = geo && 4 * RM + 16 * W >= 2 * 48 * 4 ? L.cid : take(2 * 48 * 4, 16);
@@ -242,13 +241,14 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     const uint32_t xa = XA ? extra_depth(ef, a.depth) : 0u;
     const uint32_t EFM = (ef + xa + 31u) & ~31u;
     // visited-table entry width: byte / short tags where they identify ids
-    // exactly, else full ids (the headline geometry keeps full ids: its table
-    // is small and its lossy re-evaluations are ~2 %)
-    const uint32_t vtw = GEO ? 4u : vis_tag_bytes(ix.n, a.vis_log2);
-    const uint32_t vbits = GEO ? 32u : vis_id_bits(ix.n);
+    // exactly, else full ids
+    // (the headline kernel is dispatched only when a short tag identifies ids
+    // exactly, and always keeps 2-byte entries: compile-time table code)
+    const uint32_t vtw = GEO ? 2u : vis_tag_bytes(ix.n, a.vis_log2);
+    const uint32_t vbits = vis_id_bits(ix.n);
     const uint32_t vmask = vbits >= 32 ? ~0u : (1u << vbits) - 1u;
     const uint32_t vtb = vbits > a.vis_log2 ? vbits - a.vis_log2 : 0u;  // tag bits
-    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, GEO ? 4u * VS : VS * vtw, SR, xa, true, GEO);
+    const SmemLayout L = smem_layout(EFM, RM, W, a.tie_cap, VS * vtw, SR, xa, true, GEO);
     unsigned char* base = smem_raw + (size_t)wib * warp_bytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
     unsigned char* const stage0 = base + L.stage0;
@@ -276,7 +276,14 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     // visited-table test-and-set: true if `id` was not recorded (lossy: a
     // forgotten node is only re-scored, never wrongly skipped)
     auto vis_insert = [&](uint32_t id) -> bool {
-        if constexpr (GEO) return true;  // (never called: GEO inlines the full-id table)
+        if constexpr (GEO) {
+            const uint32_t mx = (id * 0x9E3779B1u) & vmask;
+            const uint32_t s = mx >> vtb, tg = mx & ((1u << vtb) - 1u);
+            uint16_t* v16 = reinterpret_cast<uint16_t*>(vis);
+            if (v16[s] == tg) return false;
+            v16[s] = (uint16_t)tg;
+            return true;
+        }
         if (vtw == 4u) {
             const uint32_t s = vhash(id, a.vis_log2);
             if (vis[s] == id) return false;
@@ -488,13 +495,12 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             for (uint64_t i = lane; i < a.exact_words / 4; i += 32) xb4[i] = make_uint4(0, 0, 0, 0);
             __syncwarp();
         } else {
-            const uint32_t vwords = GEO ? VS : (VS * vtw) / 4u;
+            const uint32_t vwords = (VS * vtw) / 4u;
             for (uint32_t i = lane; i < vwords; i += 32) vis[i] = kSentinel;  // all 0xFF
         }
         const uint32_t entry = a.entry;
         if (lane == 0) {
             if (xbits) atomicOr(xbits + (entry >> 5), 1u << (entry & 31));
-            else if (GEO) vis[vhash(entry, a.vis_log2)] = entry;
             else vis_insert(entry);
         }
         uint32_t np = 0, tn = 0, tdist = 0, hint = 0;
@@ -1037,13 +1043,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                         const uint32_t bit = 1u << (id & 31);
                         k2 = (atomicOr(xbits + (id >> 5), bit) & bit) == 0;
                     } else {
-                        if constexpr (GEO) {  // full ids (codegen of the headline kernel kept)
-                            const uint32_t s = vhash(id, a.vis_log2);
-                            if (vis[s] == id) k2 = false;
-                            else vis[s] = id;
-                        } else {
-                            k2 = vis_insert(id);
-                        }
+                        k2 = vis_insert(id);
                     }
                 }
                 keep[j] = k2;
@@ -1348,7 +1348,7 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     const bool split = p.SR * 2u <= 32u && p.SR <= split_max_rows();
     if (relax) p.fn = pick_relaxed(p.rw, relax, split);
     else if (geo_ok && p.rw == 2 && !xa && !split && ix.W == 12 && ix.dim == 768 && p.SR == 32 &&
-             stage_half_bytes() == 6144)
+             stage_half_bytes() == 6144 && vis_tag_bytes(ix.n, vis_log2) <= 2u)
     {
         p.fn = fused ? (void*)search_kernel<2, false, false, 0, 12, true, true>
                      : (void*)search_kernel<2, false, false, 0, 12, true, false>;
@@ -1376,7 +1376,7 @@ Plan make_plan(const DevIndex& ix, uint32_t ef, uint32_t vis_log2, uint32_t tie_
     else if (p.rw == 2) p.fn = pick_kernel<2>(xa != 0, split);
     else p.fn = pick_kernel<4>(xa != 0, split);
     const SmemLayout L = smem_layout((ef + xa + 31) & ~31u, p.rw * 32, ix.W, tie_cap,
-                                     (1u << vis_log2) * (p.geo ? 4u : vis_tag_bytes(ix.n, vis_log2)),
+                                     (1u << vis_log2) * (p.geo ? 2u : vis_tag_bytes(ix.n, vis_log2)),
                                      p.SR, xa, true, p.geo);
     p.warp_bytes = L.total;
     if (p.geo || p.one) {
