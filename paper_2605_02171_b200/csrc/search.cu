@@ -101,7 +101,7 @@ __device__ __forceinline__ float dot4_exact(const float* __restrict__ q,
 }
 
 struct SmemLayout {
-    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, qsl, acd, axk,
+    uint32_t bars, stage0, stage1, pk, ctd, evk, crp, csrp, cid, stg, qc, tie, vis, qsl, qd, acd, axk,
         axr, total;
 };
 
@@ -151,6 +151,9 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     // rerank query slices (geo: over the compacted-id buffer and the query
     // code, contiguous and both dead during the rerank)
     L.qsl = geo && 4 * RM + 16 * W >= 2 * 48 * 4 ? L.cid : take(2 * 48 * 4, 16);
+    // the current rerank round's query slice as doubles (converted once per
+    // warp instead of once per lane)
+    L.qd = take(48 * 8, 16);
     // extra depth: A candidates of one step (<= RM: each scored key is a P
     // contender or an A candidate, and evictions <= P contenders), sorted copy
     // and their ranks in A
@@ -273,6 +276,8 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     uint32_t* vis = reinterpret_cast<uint32_t*>(base + L.vis);
     float* sc = reinterpret_cast<float*>(base + L.vis);
     float* qsl = reinterpret_cast<float*>(base + L.qsl);
+    double* qd = reinterpret_cast<double*>(base + L.qd);
+    (void)qd;
     // visited-table test-and-set: true if `id` was not recorded (lossy: a
     // forgotten node is only re-scored, never wrongly skipped)
     auto vis_insert = [&](uint32_t id) -> bool {
@@ -1164,28 +1169,68 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                     phs ^= 1u << h;
                     if (s == 0) s0 = s1 = s2 = s3 = 0.0;
                     const uint32_t row = 32u * g + lane;
-                    if (row < NR) {
-                        const float4* rp = reinterpret_cast<const float4*>(
-                            stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
-#pragma unroll
-                        for (uint32_t u = 0; u < kMaxSL4; ++u) {
-                            if (4u * u >= lim) break;
-                            const uint32_t i = i0 + 4u * u;
-                            const float4 v = rp[u];
-                            const float4 qq = qr[u];
-                            if (i + 4 <= main4) {
-                                s0 = __fma_rn((double)qq.x, (double)v.x, s0);
-                                s1 = __fma_rn((double)qq.y, (double)v.y, s1);
-                                s2 = __fma_rn((double)qq.z, (double)v.z, s2);
-                                s3 = __fma_rn((double)qq.w, (double)v.w, s3);
-                            } else {  // tail elements >= 4*floor(D/4) all go to s0
-                                if (i < dim) s0 = __fma_rn((double)qq.x, (double)v.x, s0);
-                                if (i + 1 < dim) s0 = __fma_rn((double)qq.y, (double)v.y, s0);
-                                if (i + 2 < dim) s0 = __fma_rn((double)qq.z, (double)v.z, s0);
-                            }
+                    if constexpr (GEO) {
+                        // D = 768: every slice is a full 48 floats of 4-element
+                        // groups.  The float -> double conversions share the
+                        // FP64 pipe with the chains: the query's are done once
+                        // per warp (two per lane) instead of 48 per lane.
+                        if (lane < 24) {
+                            const float2 f = reinterpret_cast<const float2*>(qr)[lane];
+                            reinterpret_cast<double2*>(qd)[lane] = make_double2((double)f.x, (double)f.y);
                         }
-                        if (s == nsl - 1)
-                            sc[row] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                        __syncwarp();
+                        if (row < NR) {
+                            const float4* rp = reinterpret_cast<const float4*>(
+                                stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
+                            const double2* q2 = reinterpret_cast<const double2*>(qd);
+#pragma unroll
+                            for (uint32_t u = 0; u < kMaxSL4; ++u) {
+                                const float4 v = rp[u];
+                                const double2 qa = q2[2 * u], qb = q2[2 * u + 1];
+                                s0 = __fma_rn(qa.x, (double)v.x, s0);
+                                s1 = __fma_rn(qa.y, (double)v.y, s1);
+                                s2 = __fma_rn(qb.x, (double)v.z, s2);
+                                s3 = __fma_rn(qb.y, (double)v.w, s3);
+                            }
+                            if (s == nsl - 1)
+                                sc[row] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                        }
+                        __syncwarp();  // qd is rewritten by the next round
+                    } else {
+                        // the query slice as doubles, converted once per warp
+                        // (the slice buffer holds 48 floats; values past `lim`
+                        // are never used)
+                        if (lane < 24) {
+                            const float2 f = reinterpret_cast<const float2*>(qr)[lane];
+                            reinterpret_cast<double2*>(qd)[lane] = make_double2((double)f.x, (double)f.y);
+                        }
+                        __syncwarp();
+                        const double2* q2 = reinterpret_cast<const double2*>(qd);
+                        if (row < NR) {
+                            const float4* rp = reinterpret_cast<const float4*>(
+                                stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
+#pragma unroll
+                            for (uint32_t u = 0; u < kMaxSL4; ++u) {
+                                if (4u * u >= lim) break;
+                                const uint32_t i = i0 + 4u * u;
+                                const float4 v = rp[u];
+                                const double2 qa = q2[2 * u], qb = q2[2 * u + 1];
+                                const double qx = qa.x, qy = qa.y, qz = qb.x, qw = qb.y;
+                                if (i + 4 <= main4) {
+                                    s0 = __fma_rn(qx, (double)v.x, s0);
+                                    s1 = __fma_rn(qy, (double)v.y, s1);
+                                    s2 = __fma_rn(qz, (double)v.z, s2);
+                                    s3 = __fma_rn(qw, (double)v.w, s3);
+                                } else {  // tail elements >= 4*floor(D/4) all go to s0
+                                    if (i < dim) s0 = __fma_rn(qx, (double)v.x, s0);
+                                    if (i + 1 < dim) s0 = __fma_rn(qy, (double)v.y, s0);
+                                    if (i + 2 < dim) s0 = __fma_rn(qz, (double)v.z, s0);
+                                }
+                            }
+                            if (s == nsl - 1)
+                                sc[row] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                        }
+                        __syncwarp();  // qd is rewritten by the next round
                     }
                     if (t + 2 < rounds) rr_issue(t + 2);
                 }
