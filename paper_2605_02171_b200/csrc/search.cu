@@ -153,7 +153,9 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t EFM, uint32_t RM, uin
     L.qsl = geo && 4 * RM + 16 * W >= 2 * 48 * 4 ? L.cid : take(2 * 48 * 4, 16);
     // the current rerank round's query slice as doubles (converted once per
     // warp instead of once per lane)
-    L.qd = take(48 * 8, 16);
+    // (outside geo the contender buffer is ordinary shared memory, dead during
+    // the rerank)
+    L.qd = !geo && 8 * RM >= 48 * 8 ? L.ctd : take(48 * 8, 16);
     // extra depth: A candidates of one step (<= RM: each scored key is a P
     // contender or an A candidate, and evictions <= P contenders), sorted copy
     // and their ranks in A
