@@ -156,3 +156,34 @@ def test_narrow_rows_rerank_more_than_32_rows(dim):
         for ex in (True, False):
             r = ix.search_ex(q, k=10, ef=ef, exact_visited=ex)
             _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, (dim, ef, ex))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nq", [1, 100, 300])
+def test_pinned_result_buffers_are_written_by_the_kernel(nq):
+    """Result buffers in pinned host memory are written by the search kernel
+    through their device alias (no staging copy): the latency kernel (small
+    batches), the per-warp kernel, and the pipelined host-query path must
+    deliver the same ids / score bits / counts as the reference."""
+    import torch
+    ref, ix, q = _ref_graph(768)
+    q = q[:nq]
+    rid, rsc, rcnt = ref.run_query_batch(q, 64, 10, threads=THREADS)
+    for src in ("pageable", "pinned", "device"):
+        qq = {"pageable": q, "pinned": torch.from_numpy(q).pin_memory(),
+              "device": torch.from_numpy(q).cuda()}[src]
+        ids = torch.full((nq, 10), -7, dtype=torch.int32).pin_memory()
+        sc = torch.full((nq, 10), -7.0, dtype=torch.float32).pin_memory()
+        cnt = torch.full((nq,), -7, dtype=torch.int32).pin_memory()
+        ix.search(qq, k=10, ef=64, out=(ids, sc, cnt))
+        _same(ids.numpy().view(np.uint32), sc.numpy(), cnt.numpy().view(np.uint32),
+              rid, rsc, rcnt, (nq, src))
+    # a larger batch: pipelined upload + fused prologue writing pinned results
+    big = np.tile(q, (max(1, 2100 // nq) + 1, 1))[:2100]
+    bid, bsc, bcnt = ref.run_query_batch(big, 32, 10, threads=THREADS)
+    ids = torch.empty((2100, 10), dtype=torch.int32).pin_memory()
+    sc = torch.empty((2100, 10), dtype=torch.float32).pin_memory()
+    cnt = torch.empty((2100,), dtype=torch.int32).pin_memory()
+    ix.search(torch.from_numpy(big).pin_memory(), k=10, ef=32, out=(ids, sc, cnt))
+    _same(ids.numpy().view(np.uint32), sc.numpy(), cnt.numpy().view(np.uint32),
+          bid, bsc, bcnt, (nq, "pipelined"))
