@@ -412,9 +412,10 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
     // each cudaMemcpyAsync, so its chunks are submitted after the launch (the
     // kernel runs while the driver stages them); under such tools use
     // QVG_PIPELINE=0 for pageable host queries.
-    // (a ramped schedule — 128 / 256 / 512-query first chunks, only the first
-    // submitted before the launch — measured 0.4 % slower end to end than
-    // uniform chunks submitted first: profiles/r2k_e2e_ab.txt)
+    // (launching before the copies are queued — only a first chunk of 128 to
+    // 1024 queries submitted ahead of the kernel, ramped or not, polling every
+    // 256 ns or 2 us — measured 0.4-1.7 % slower end to end than every chunk
+    // submitted first: profiles/r2k_e2e_ab.txt, r2w_early_ab.txt)
     const bool copies_first = pipelined && (is_pinned_host_ptr(user_in) || under_tool());
     uint64_t next_c0 = 0, next_c = 0;
     bool chunks_started = false;

@@ -187,3 +187,32 @@ def test_pinned_result_buffers_are_written_by_the_kernel(nq):
     ix.search(torch.from_numpy(big).pin_memory(), k=10, ef=32, out=(ids, sc, cnt))
     _same(ids.numpy().view(np.uint32), sc.numpy(), cnt.numpy().view(np.uint32),
           bid, bsc, bcnt, (nq, "pipelined"))
+
+
+@pytest.mark.gpu
+def test_pinned_result_buffers_with_tie_spill_rerun():
+    """qvg_search_ex with pinned result / status buffers and a 4-entry tie
+    stack on the tie-saturated graph: the overflowed queries are re-run with the
+    global-memory stack and the kernel-written pinned buffers hold the
+    reference's answers."""
+    import ctypes as C
+
+    import torch
+    from paper_2605_02171_b200 import _native as N
+    ref, ix, q = _tie_saturated()
+    nq = q.shape[0]
+    rid, rsc, rcnt = ref.run_query_batch(q, 16, 10, threads=THREADS)
+    ids = torch.full((nq, 10), -7, dtype=torch.int32).pin_memory()
+    sc = torch.full((nq, 10), -7.0, dtype=torch.float32).pin_memory()
+    cnt = torch.full((nq,), -7, dtype=torch.int32).pin_memory()
+    qs = torch.full((nq,), -7, dtype=torch.int32).pin_memory()
+    opts = N.qvg_search_opts(tie_capacity=4, entry_point=Q.SENTINEL)
+    st = N.qvg_stats()
+    rc = N.lib().qvg_search_ex(ix._h, q.ctypes.data, nq, 10, 16, C.byref(opts), ids.data_ptr(),
+                               sc.data_ptr(), cnt.data_ptr(), qs.data_ptr(), None, None, None,
+                               None, C.byref(st))
+    assert rc == 0, N.last_error()
+    assert st.tie_overflows > 0, "test graph does not exercise the spill"
+    assert (qs.numpy() == 0).all()
+    _same(ids.numpy().view(np.uint32), sc.numpy(), cnt.numpy().view(np.uint32), rid, rsc, rcnt,
+          "pinned + spill")
