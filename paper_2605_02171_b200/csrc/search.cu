@@ -391,6 +391,13 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             float* row = reinterpret_cast<float*>(stage0);
             const float* src = a.qraw + q * ix.dim;
             const uint32_t dim = ix.dim;
+            // when the stage also holds the row as doubles (12 B per element),
+            // all lanes convert in parallel and lane 0's chains read doubles:
+            // 48 warp-wide conversions per query instead of 1536 single-lane
+            // ones on the FP64-class pipe the reranking warps also need
+            const uint32_t xd_off = (4u * dim + 15u) & ~15u;
+            const bool use_xd = xd_off + 8u * dim <= 2u * (SR / 4u) * gstride;
+            double* xd = reinterpret_cast<double*>(stage0 + xd_off);
             bool fin = true;
             for (uint32_t i = lane; i < dim; i += 32) {
                 // L2-only load: with a pipelined upload the row may have been
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 const float v = __ldcg(src + i);
                 fin &= isfinite(v);
                 row[i] = v;
+                if (use_xd) xd[i] = (double)v;
             }
             fin = __all_sync(kFull, fin);
             __syncwarp();
@@ -406,6 +414,16 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             if (lane == 0 && qst == QVG_Q_OK) {
                 double acc = 0.0;
                 uint32_t i = 0;
+                if (use_xd) {
+                    for (; i + 8 <= dim; i += 8) {
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v[u] = xd[i + u];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc = __fma_rn(v[u], v[u], acc);
+                    }
+                    for (; i < dim; ++i) acc = __fma_rn(xd[i], xd[i], acc);
+                }
                 for (; i + 8 <= dim; i += 8) {
                     float v[8];
 #pragma unroll
@@ -425,7 +443,10 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             for (uint32_t i = lane; i < ix.Dp; i += 32) {
                 const float y = (i < dim && qst == QVG_Q_OK) ? __fmul_rn(row[i], inv) : 0.0f;
                 yfin &= isfinite(y);
-                if (i < dim) row[i] = y;
+                if (i < dim) {
+                    row[i] = y;
+                    if (use_xd) xd[i] = fabs((double)y);
+                }
                 qout[i] = y;
             }
             yfin = __all_sync(kFull, yfin);
@@ -435,6 +456,16 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             if (lane == 0 && qst == QVG_Q_OK) {
                 double s = 0.0;
                 uint32_t i = 0;
+                if (use_xd) {
+                    for (; i + 8 <= dim; i += 8) {
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v[u] = xd[i + u];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+                    }
+                    for (; i < dim; ++i) s = __dadd_rn(s, xd[i]);
+                }
                 for (; i + 8 <= dim; i += 8) {
                     float v[8];
 #pragma unroll
