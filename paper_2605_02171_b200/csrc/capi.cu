@@ -336,6 +336,41 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         a.exact_words = words;
     }
 
+    // ---- tail balancing (headline-geometry kernel; see SearchLaunch) ----------
+    {
+        static const bool susp_env = [] {  // QVG_SUSPEND=0: whole queries only (A/B)
+            const char* v = getenv("QVG_SUSPEND");
+            return !(v && v[0] == '0');
+        }();
+        const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
+        const uint64_t slots = grid * wpb;
+        // (ef < 32: a query is ~50 us, a hand-off ~3 us: whole queries win, ef 16 -1.7 %)
+        if (susp_env && pinfo.susp_blob_bytes && !exact && !relax && !xa && h->has_tmap &&
+            ef >= 32 && nq > slots && nq < (1ull << 31)) {
+            // the last round's queries (one per warp slot) run in units of about a
+            // quarter of a query
+            const uint64_t nb = nq < slots ? nq : slots;
+            const uint32_t stride16 = (64u + pinfo.susp_blob_bytes + 15u) / 16u;
+            const uint64_t cap = 8 * nb + 64;
+            const size_t head = 64 + ((cap * 4 + 15) & ~size_t(15));
+            if ((st = grow(h->s_susp, head + nb * stride16 * 16ull)) != QVG_OK) return st;
+            char* p = static_cast<char*>(h->s_susp.p);
+            a.susp_ctl = reinterpret_cast<uint32_t*>(p);
+            a.susp_list = reinterpret_cast<uint32_t*>(p + 64);
+            a.susp_state = reinterpret_cast<uint4*>(p + head);
+            a.susp_from = (uint32_t)(nq - nb);
+            // (cfg 2, ef 64, kernel ms: off 2.080; window of 0.5 / 1 / 1.5 / 2 / 3 / 4
+            // rounds at this budget 2.027 / 1.971 / 1.972 / 1.988 / 1.992 / 2.011;
+            // budgets of 12 / 16 / 21 / 30 / 40 / 55 expansions at 1 round
+            // - / - / 1.971 / 1.985 / 1.987 / 2.022: profiles/r3_susp_tune*.txt)
+            a.susp_budget = (3u * ef + 9u) / 10u + 2u;
+            if (a.susp_budget < 12u) a.susp_budget = 12u;
+            a.susp_cap = (uint32_t)cap;
+            a.susp_stride16 = stride16;
+            cudaMemsetAsync(p, 0, head, s);
+        }
+    }
+
     // ---- pipeline -------------------------------------------------------------
     uint32_t* d_flags = reinterpret_cast<uint32_t*>(static_cast<char*>(h->s_counter.p) + 32);
     uint32_t* d_ready = reinterpret_cast<uint32_t*>(static_cast<char*>(h->s_counter.p) + 48);
@@ -523,6 +558,7 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
                               nullptr, static_cast<int32_t*>(h->s_qst.p), nullptr, s);
             }
             SearchLaunch r = a;
+            r.susp_ctl = nullptr;
             r.qraw = nullptr;
             r.qn_out = nullptr;
             r.ready = nullptr;
@@ -615,6 +651,10 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         stats->tie_overflows = n_spilled;  // re-run with a global-memory tie stack
     }
     if (hflags == 0) return QVG_OK;
+    if (hflags & (1u << 30)) {
+        set_error("search: internal error (a suspended query was never handed over)");
+        return QVG_RUNTIME_ERROR;
+    }
     // rare path: locate the first offending query (the reference's
     // single-threaded batch throws at the first invalid one)
     std::vector<int32_t> qs(nq);

@@ -77,7 +77,8 @@ void free_index(qvg_index* h) {
     cudaFree(h->d_cold);
     Buffer* bufs[] = {&h->s_in,   &h->s_qn,     &h->s_qc,     &h->s_qst,    &h->s_ids,
                       &h->s_sc,   &h->s_cnt,    &h->s_pool_i, &h->s_pool_d, &h->s_pool_n,
-                      &h->s_qctr, &h->s_counter, &h->s_exact, &h->s_pair_ids, &h->s_pair_out, &h->s_st};
+                      &h->s_qctr, &h->s_counter, &h->s_exact, &h->s_pair_ids, &h->s_pair_out, &h->s_st,
+                      &h->s_susp};
     for (Buffer* b : bufs) cudaFree(b->p);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);

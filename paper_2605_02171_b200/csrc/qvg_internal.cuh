@@ -41,6 +41,9 @@ struct Buffer {
 struct PlanInfo {
     uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0, sms = 0;
     uint64_t coop_cap = 0;  // resident CTAs of the latency kernel (0 = n/a)
+    // headline-geometry kernel: bytes of per-query search state a warp saves
+    // when it suspends a query (0 = the planned kernel cannot suspend)
+    uint32_t susp_blob_bytes = 0;
 };
 
 }  // namespace qvg
@@ -57,7 +60,7 @@ struct qvg_index {
     void* d_cold = nullptr;
     // scratch, grown on demand
     qvg::Buffer s_in, s_qn, s_qc, s_qst, s_ids, s_sc, s_cnt, s_pool_i, s_pool_d, s_pool_n,
-        s_qctr, s_counter, s_exact, s_pair_ids, s_pair_out, s_st;
+        s_qctr, s_counter, s_exact, s_pair_ids, s_pair_out, s_st, s_susp;
     cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     // pipelined upload of host queries (created on first use): copy stream,
     // its completion event, pinned ready counts published after each chunk
@@ -143,6 +146,18 @@ struct SearchLaunch {
     uint64_t* exp_out;
     uint32_t* exp_n;
     uint32_t exp_cap;
+    // Tail balancing (headline-geometry kernel only; null = off).  The last
+    // queries of a batch (index >= susp_from) run in units of susp_budget
+    // expansions: at the end of a unit the warp saves the query's search state
+    // (pool, compacted rows, query code, tie stack, visited table, scalars) to
+    // susp_state and appends the query to a FIFO that warps serve once the fresh
+    // queries are gone.  The batch then ends with every warp on a short unit
+    // instead of a fifth of them on a whole query; results are unchanged (the
+    // state machine resumes where it stopped).
+    uint32_t* susp_ctl;     // [0] pushes reserved, [1] pops reserved, [2] budgeted queries completed
+    uint32_t* susp_list;    // susp_cap entries, zeroed per launch; entry = query + 1
+    uint4* susp_state;      // susp_stride16 uint4 per budgeted query
+    uint32_t susp_from, susp_budget, susp_cap, susp_stride16;
 };
 
 // Visited-table entry width (bytes) for n nodes and 2^lg slots.  The table

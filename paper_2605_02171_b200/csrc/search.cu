@@ -367,10 +367,42 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         unsigned long long qq = 0;
         if (lane == 0) qq = atomicAdd(a.counter, 1ull);
         qq = __shfl_sync(kFull, qq, 0);
-        if (qq >= a.nq) break;
+        bool resume = false;  // this unit continues a suspended query (GEO only)
+        if (qq >= a.nq) {
+            if (!(GEO && a.susp_ctl)) break;
+            // fresh queries are gone: serve the FIFO of suspended queries until
+            // every budgeted query has completed
+            uint32_t ent = 0;
+            if (lane == 0) {
+                const uint32_t slot = atomicAdd(a.susp_ctl + 1, 1u);
+                const uint32_t nb = (uint32_t)a.nq - a.susp_from;
+                if (slot < a.susp_cap) {
+                    for (uint32_t spins = 0; spins < (1u << 24); ++spins) {  // (bounded: ~4 s)
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ent) : "l"(a.susp_list + slot) : "memory");
+                        if (ent) break;
+                        uint32_t done;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(a.susp_ctl + 2) : "memory");
+                        if (done >= nb) {  // no push can follow: a last look at the slot
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ent) : "l"(a.susp_list + slot) : "memory");
+                            break;
+                        }
+                        __nanosleep(200);
+                        // (never seen: a watchdog so a lost hand-off fails the call
+                        // instead of hanging it)
+                        if (spins + 1 == (1u << 24) && a.flags) atomicOr(a.flags, 1u << 30);
+                    }
+                }
+            }
+            ent = __shfl_sync(kFull, ent, 0);
+            __syncwarp();  // lane 0's acquire orders every lane's reads of the saved state
+            if (ent == 0) break;
+            qq = ent - 1u;
+            resume = true;
+        }
         // a re-run launch serves a list of queries (qmap), never a LEAN kernel
         const uint64_t q = (!LEAN && a.qmap) ? (uint64_t)a.qmap[qq] : qq;
-        if (a.ready) {  // pipelined upload: wait until this query's row has landed
+        const bool budgeted = GEO && a.susp_ctl && q >= a.susp_from;
+        if (a.ready && !resume) {  // pipelined upload: wait until this query's row has landed
             if (lane == 0) {
                 uint32_t r;
                 for (;;) {
@@ -383,7 +415,9 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         }
 
         int32_t qst = 0;
-        if (PRO && a.qraw) {
+        if (resume) {
+            // (encoded, validated and initialised by the unit that started it)
+        } else if (PRO && a.qraw) {
             // fused K1 (encode.cu semantics, bit-exact): the stage is idle
             // between queries and holds the raw row; lane 0 runs the two
             // index-ordered double reductions (vec_math.hpp:28-44,
@@ -514,6 +548,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 if (a.pool_n) a.pool_n[q] = 0;
                 if (a.qctr)
                     for (int i = 0; i < 8; ++i) a.qctr[q * 8 + i] = i == 7 ? (uint32_t)qst : 0u;
+                if (budgeted) atomicAdd(a.susp_ctl + 2, 1u);
             }
             continue;
         }
@@ -526,9 +561,10 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         unsigned long long tg0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
 #endif
-        if (!a.qraw)
+        if (!a.qraw && !resume)
             for (uint32_t w = lane; w < W; w += 32) qc[w] = a.qcodes[q * W + w];
-        if (xbits) {
+        if (resume) {
+        } else if (xbits) {
             uint4* xb4 = reinterpret_cast<uint4*>(xbits);
             for (uint64_t i = lane; i < a.exact_words / 4; i += 32) xb4[i] = make_uint4(0, 0, 0, 0);
             __syncwarp();
@@ -537,7 +573,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             for (uint32_t i = lane; i < vwords; i += 32) vis[i] = kSentinel;  // all 0xFF
         }
         const uint32_t entry = a.entry;
-        if (lane == 0) {
+        if (lane == 0 && !resume) {
             if (xbits) atomicOr(xbits + (entry >> 5), 1u << (entry & 31));
             else vis_insert(entry);
         }
@@ -549,7 +585,25 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         uint32_t c_mtot = 0;  // contenders per query (diagnostics)
 #endif
         uint32_t n = 1;  // rows to score in cid[0..n)
-        if (lane == 0) cid[0] = entry;
+        if (lane == 0 && !resume) cid[0] = entry;
+        // suspended-query state: a 64-B header of scalars, then the shared-memory
+        // range [pk, qd) (pool, compacted rows, query code, tie stack, visited table)
+        // budget_left: expansions left in this unit (~0u: unlimited; kSuspended: handed over)
+        constexpr uint32_t kSuspended = 0xFFFFFFFEu;
+        uint32_t budget_left = ~0u;
+        if constexpr (GEO) {
+            if (budgeted) budget_left = a.susp_budget;
+            if (resume) {
+                const uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
+                const uint32_t blob16 = (L.qd - L.pk) / 16u;
+                uint4* dst = reinterpret_cast<uint4*>(base + L.pk);
+                for (uint32_t i = lane; i < blob16; i += 32) dst[i] = __ldcg(sstate + 4 + i);
+                const uint4 h0 = __ldcg(sstate), h1 = __ldcg(sstate + 1), h2 = __ldcg(sstate + 2);
+                np = h0.x, tn = h0.y, tdist = h0.z, hint = h0.w;
+                n = h1.x, c_exp = h1.y, c_tie = h1.z, c_eval = h1.w;
+                c_drop = lane == 0 ? h2.x : 0u, c_slots = h2.y, c_maxtie = h2.z, overflow = h2.w != 0;
+            }
+        }
         __syncwarp();
         uint32_t spec_u = kSentinel;  // speculatively prefetched adjacency row
         uint64_t spec_key = kInfKey;  // its key (the predicted next pick)
@@ -604,6 +658,34 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0, ph_tma = 0;)
         for (;;) {
             QVG_PH(long long tp0 = clock64();)
+            if constexpr (GEO) {
+                if (budget_left == 0) {
+                    // end of this unit: save the state and hand the query to the FIFO
+                    // (a full FIFO just lets this warp finish the query)
+                    uint32_t slot = 0;
+                    if (lane == 0) slot = atomicAdd(a.susp_ctl, 1u);
+                    slot = __shfl_sync(kFull, slot, 0);
+                    if (slot < a.susp_cap) {
+                        uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
+                        const uint32_t blob16 = (L.qd - L.pk) / 16u;
+                        const uint4* src = reinterpret_cast<const uint4*>(base + L.pk);
+                        for (uint32_t i = lane; i < blob16; i += 32) __stcg(sstate + 4 + i, src[i]);
+                        for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
+                        if (lane == 0) {
+                            __stcg(sstate, make_uint4(np, tn, tdist, hint));
+                            __stcg(sstate + 1, make_uint4(n, c_exp, c_tie, c_eval));
+                            __stcg(sstate + 2, make_uint4(c_drop, c_slots, c_maxtie, overflow ? 1u : 0u));
+                        }
+                        __threadfence();
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.susp_list + slot), "r"((uint32_t)q + 1u) : "memory");
+                        budget_left = kSuspended;
+                        break;
+                    }
+                    budget_left = ~0u;
+                }
+            }
             c_eval += n;
             // (a) TMA-gather the code rows (double-buffered halves of SR rows)
             const uint32_t nsub = __umulhi(n + SR - 1, sr_m);  // (n + SR - 1) / SR
@@ -1039,6 +1121,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             if (!LEAN && !REL && a.exp_out && lane == 0 && c_exp < a.exp_cap)
                 a.exp_out[q * a.exp_cap + c_exp] = ordk(spec_key);
             if (!REL) ++c_exp;
+            if (GEO && budget_left != ~0u) --budget_left;  // (a unit's budget is far below kSuspended)
 
             // (g) adjacency row (stored order): the speculative prefetch when it
             // guessed right, else a fresh vectorised load
@@ -1104,6 +1187,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             QVG_PH(ph_pick += clock64() - tp3;)
         }
 
+        if (GEO && budget_left == kSuspended) continue;
         // ---- outputs ------------------------------------------------------------
         const long long t_search = kTimers ? clock64() : 0;
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
@@ -1321,6 +1405,10 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             a.qctr[q * 8 + 4] = c_mtot;
         }
 #endif
+        if (GEO && a.susp_ctl && q >= a.susp_from && lane == 0) {  // (the FIFO servers exit on this count)
+            __threadfence();
+            atomicAdd(a.susp_ctl + 2, 1u);
+        }
         __syncwarp();
     }
 }
@@ -1601,6 +1689,11 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         info->smem_per_block = p.block_bytes;
         info->resident_warps_per_sm = (uint32_t)per_sm * p.wpb;
         info->sms = (uint32_t)sms;
+        if (p.geo) {  // [pk, qd): pool, compacted ids, query code, tie stack, visited table
+            const SmemLayout L = smem_layout((a.ef + xa + 31) & ~31u, p.rw * 32, a.ix.W, a.tie_cap,
+                                             (1u << a.vis_log2) * 2u, p.SR, xa, true, true);
+            info->susp_blob_bytes = L.qd - L.pk;
+        }
     }
     return QVG_OK;
 }

@@ -216,3 +216,38 @@ def test_pinned_result_buffers_with_tie_spill_rerun():
     assert (qs.numpy() == 0).all()
     _same(ids.numpy().view(np.uint32), sc.numpy(), cnt.numpy().view(np.uint32), rid, rsc, rcnt,
           "pinned + spill")
+
+
+# ------------------------------------------------ tail balancing (suspended queries)
+@pytest.mark.gpu
+@pytest.mark.parametrize("ef", [32, 64, 130])
+def test_tail_balancing_units_resume_exactly(ef):
+    """Batches larger than one round of warp slots on the headline geometry
+    (D = 768, R = 64) run their last round in units: a warp saves the query's
+    search state after a budget of expansions and any warp resumes it later.
+    Results, pools and expansion counters must equal the reference / the
+    whole-query exact-visited path, for device queries and the pipelined host
+    path (fused prologue)."""
+    import torch
+    from workloads.datasets import mixture
+    ref, ix, _ = _ref_graph(768)
+    _, q = mixture(3_000, 768, 60, 0.3, seed=768, nq=5200, sigma_mode="norm")
+    rid, rsc, rcnt = ref.run_query_batch(q, ef, 10, threads=THREADS)
+    r = ix.search_ex(torch.from_numpy(q).cuda(), k=10, ef=ef)
+    wpb = r["stats"]["warps_per_block"]
+    assert wpb >= 13, "headline-geometry kernel (one block per SM) expected"
+    assert q.shape[0] > r["stats"]["grid_blocks"] * wpb, "batch must exceed one round of warp slots"
+    _same(r["ids"], r["scores"], r["count"], rid, rsc, rcnt, (ef, "device"))
+    x = ix.search_ex(q, k=10, ef=ef, exact_visited=True)  # whole queries, other kernel
+    assert np.array_equal(r["pool_ids"], x["pool_ids"]) and np.array_equal(r["pool_dists"], x["pool_dists"])
+    assert np.array_equal(r["counters"][:, :2], x["counters"][:, :2])  # expansions, tie expansions
+    assert (r["status"] == 0).all()
+    ids, sc, cnt = ix.search(q, k=10, ef=ef)  # host queries: pipelined upload + fused prologue
+    _same(ids, sc, cnt, rid, rsc, rcnt, (ef, "host"))
+    bad = q.copy()
+    bad[[7, 4000, 5100]] = 0.0  # zero-norm rows, one of them in the unit-budgeted tail
+    rb = ix.search_ex(bad, k=10, ef=ef, check=False)
+    ok = np.ones(len(bad), bool)
+    ok[[7, 4000, 5100]] = False
+    assert (rb["status"][~ok] != 0).all() and (rb["status"][ok] == 0).all()
+    _same(rb["ids"][ok], rb["scores"][ok], rb["count"][ok], rid[ok], rsc[ok], rcnt[ok], (ef, "bad rows"))
