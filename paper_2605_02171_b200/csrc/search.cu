@@ -588,9 +588,12 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         if (lane == 0 && !resume) cid[0] = entry;
         // suspended-query state: a 64-B header of scalars, then the shared-memory
         // range [pk, qd) (pool, compacted rows, query code, tie stack, visited table)
-        // budget_left: expansions left in this unit (~0u: unlimited; kSuspended: handed over)
-        constexpr uint32_t kSuspended = 0xFFFFFFFEu;
-        uint32_t budget_left = ~0u;
+        // budget_left: expansions left in this unit (kNoBudget: whole query).  It
+        // is 0 after the loop exactly when the query was handed over: the hand-over
+        // happens at the top of an iteration, before that iteration's pick could
+        // end the search, and nothing decrements it after the final pick
+        constexpr uint32_t kNoBudget = 0x7FFFFFFFu;
+        uint32_t budget_left = kNoBudget;
         if constexpr (GEO) {
             if (budgeted) budget_left = a.susp_budget;
             if (resume) {
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         for (;;) {
             QVG_PH(long long tp0 = clock64();)
             if constexpr (GEO) {
-                if (budget_left == 0) {
+                if (__builtin_expect(budget_left == 0, 0)) {
                     // end of this unit: save the state and hand the query to the FIFO
                     // (a full FIFO just lets this warp finish the query)
                     uint32_t slot = 0;
@@ -680,10 +683,9 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                         __syncwarp();
                         if (lane == 0)
                             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.susp_list + slot), "r"((uint32_t)q + 1u) : "memory");
-                        budget_left = kSuspended;
                         break;
                     }
-                    budget_left = ~0u;
+                    budget_left = kNoBudget;
                 }
             }
             c_eval += n;
@@ -1121,7 +1123,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             if (!LEAN && !REL && a.exp_out && lane == 0 && c_exp < a.exp_cap)
                 a.exp_out[q * a.exp_cap + c_exp] = ordk(spec_key);
             if (!REL) ++c_exp;
-            if (GEO && budget_left != ~0u) --budget_left;  // (a unit's budget is far below kSuspended)
+            if (GEO) --budget_left;
 
             // (g) adjacency row (stored order): the speculative prefetch when it
             // guessed right, else a fresh vectorised load
@@ -1187,7 +1189,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             QVG_PH(ph_pick += clock64() - tp3;)
         }
 
-        if (GEO && budget_left == kSuspended) continue;
+        if (GEO && budget_left == 0) continue;
         // ---- outputs ------------------------------------------------------------
         const long long t_search = kTimers ? clock64() : 0;
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
