@@ -41,8 +41,8 @@ struct Buffer {
 struct PlanInfo {
     uint32_t warps_per_block = 0, smem_per_block = 0, resident_warps_per_sm = 0, sms = 0;
     uint64_t coop_cap = 0;  // resident CTAs of the latency kernel (0 = n/a)
-    // headline-geometry kernel: bytes of per-query search state a warp saves
-    // when it suspends a query (0 = the planned kernel cannot suspend)
+    // bytes of per-query search state a warp saves when it suspends a query
+    // (0 = the planned kernel cannot suspend)
     uint32_t susp_blob_bytes = 0;
 };
 
@@ -146,7 +146,8 @@ struct SearchLaunch {
     uint64_t* exp_out;
     uint32_t* exp_n;
     uint32_t exp_cap;
-    // Tail balancing (headline-geometry kernel only; null = off).  The last
+    // Tail balancing (exact per-warp kernels without extra rerank depth; null =
+    // off).  The last
     // queries of a batch (index >= susp_from) run in units of susp_budget
     // expansions: at the end of a unit the warp saves the query's search state
     // (pool, compacted rows, query code, tie stack, visited table, scalars) to

@@ -324,6 +324,12 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     // x / SR == __umulhi(x, sr_m) for x < 2^32 / SR (x <= a few hundred here)
     const uint32_t sr_m = 0xFFFFFFFFu / SR + 1u;
     constexpr bool ctd_prefetch = true;  // prefetch the best contender's adjacency row
+    // tail balancing (SearchLaunch::susp_*): the saved state is the contiguous
+    // shared-memory range from the pool to the end of the visited table
+    // (compiled only into the one-block-per-SM kernels: in the R = 32 kernels the
+    // extra live state cost 5 % and their ~100-us queries gain nothing from units)
+    constexpr bool SUSP = (GEO || ONE) && !REL && !XA;
+    const uint32_t susp_end = GEO ? L.qd : L.qsl;
 
     if (lane == 0) {
         mbar_init(&bars[0]);
@@ -367,9 +373,9 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         unsigned long long qq = 0;
         if (lane == 0) qq = atomicAdd(a.counter, 1ull);
         qq = __shfl_sync(kFull, qq, 0);
-        bool resume = false;  // this unit continues a suspended query (GEO only)
+        bool resume = false;  // this unit continues a suspended query
         if (qq >= a.nq) {
-            if (!(GEO && a.susp_ctl)) break;
+            if (!(SUSP && a.susp_ctl)) break;
             // fresh queries are gone: serve the FIFO of suspended queries until
             // every budgeted query has completed
             uint32_t ent = 0;
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         }
         // a re-run launch serves a list of queries (qmap), never a LEAN kernel
         const uint64_t q = (!LEAN && a.qmap) ? (uint64_t)a.qmap[qq] : qq;
-        const bool budgeted = GEO && a.susp_ctl && q >= a.susp_from;
+        const bool budgeted = SUSP && a.susp_ctl && q >= a.susp_from;
         if (a.ready && !resume) {  // pipelined upload: wait until this query's row has landed
             if (lane == 0) {
                 uint32_t r;
@@ -594,11 +600,11 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         // end the search, and nothing decrements it after the final pick
         constexpr uint32_t kNoBudget = 0x7FFFFFFFu;
         uint32_t budget_left = kNoBudget;
-        if constexpr (GEO) {
+        if constexpr (SUSP) {
             if (budgeted) budget_left = a.susp_budget;
             if (resume) {
                 const uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
-                const uint32_t blob16 = (L.qd - L.pk) / 16u;
+                const uint32_t blob16 = (susp_end - L.pk) / 16u;
                 uint4* dst = reinterpret_cast<uint4*>(base + L.pk);
                 for (uint32_t i = lane; i < blob16; i += 32) dst[i] = __ldcg(sstate + 4 + i);
                 const uint4 h0 = __ldcg(sstate), h1 = __ldcg(sstate + 1), h2 = __ldcg(sstate + 2);
@@ -661,7 +667,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
         QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0, ph_tma = 0;)
         for (;;) {
             QVG_PH(long long tp0 = clock64();)
-            if constexpr (GEO) {
+            if constexpr (SUSP) {
                 if (__builtin_expect(budget_left == 0, 0)) {
                     // end of this unit: save the state and hand the query to the FIFO
                     // (a full FIFO just lets this warp finish the query)
@@ -670,7 +676,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                     slot = __shfl_sync(kFull, slot, 0);
                     if (slot < a.susp_cap) {
                         uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
-                        const uint32_t blob16 = (L.qd - L.pk) / 16u;
+                        const uint32_t blob16 = (susp_end - L.pk) / 16u;
                         const uint4* src = reinterpret_cast<const uint4*>(base + L.pk);
                         for (uint32_t i = lane; i < blob16; i += 32) __stcg(sstate + 4 + i, src[i]);
                         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
@@ -1123,7 +1129,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             if (!LEAN && !REL && a.exp_out && lane == 0 && c_exp < a.exp_cap)
                 a.exp_out[q * a.exp_cap + c_exp] = ordk(spec_key);
             if (!REL) ++c_exp;
-            if (GEO) --budget_left;
+            if (SUSP) --budget_left;
 
             // (g) adjacency row (stored order): the speculative prefetch when it
             // guessed right, else a fresh vectorised load
@@ -1189,7 +1195,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             QVG_PH(ph_pick += clock64() - tp3;)
         }
 
-        if (GEO && budget_left == 0) continue;
+        if (SUSP && budget_left == 0) continue;
         // ---- outputs ------------------------------------------------------------
         const long long t_search = kTimers ? clock64() : 0;
         for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
@@ -1407,7 +1413,7 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             a.qctr[q * 8 + 4] = c_mtot;
         }
 #endif
-        if (GEO && a.susp_ctl && q >= a.susp_from && lane == 0) {  // (the FIFO servers exit on this count)
+        if (SUSP && a.susp_ctl && q >= a.susp_from && lane == 0) {  // (the FIFO servers exit on this count)
             __threadfence();
             atomicAdd(a.susp_ctl + 2, 1u);
         }
@@ -1691,10 +1697,12 @@ qvg_status plan_search(const SearchLaunch& a, int device, uint64_t* grid_out, Pl
         info->smem_per_block = p.block_bytes;
         info->resident_warps_per_sm = (uint32_t)per_sm * p.wpb;
         info->sms = (uint32_t)sms;
-        if (p.geo) {  // [pk, qd): pool, compacted ids, query code, tie stack, visited table
-            const SmemLayout L = smem_layout((a.ef + xa + 31) & ~31u, p.rw * 32, a.ix.W, a.tie_cap,
-                                             (1u << a.vis_log2) * 2u, p.SR, xa, true, true);
-            info->susp_blob_bytes = L.qd - L.pk;
+        if ((p.geo || p.one) && !xa && !a.relax) {  // pool .. visited table: a suspended query's state
+            const SmemLayout L =
+                smem_layout((a.ef + 31) & ~31u, p.rw * 32, a.ix.W, a.tie_cap,
+                            (1u << a.vis_log2) * (p.geo ? 2u : vis_tag_bytes(a.ix.n, a.vis_log2)),
+                            p.SR, 0, true, p.geo);
+            info->susp_blob_bytes = (p.geo ? L.qd : L.qsl) - L.pk;
         }
     }
     return QVG_OK;
