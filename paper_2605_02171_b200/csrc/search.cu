@@ -328,7 +328,11 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
     // shared-memory range from the pool to the end of the visited table
     // (compiled only into the one-block-per-SM kernels: in the R = 32 kernels the
     // extra live state cost 5 % and their ~100-us queries gain nothing from units)
+#ifdef QVG_NOSUSP
+    constexpr bool SUSP = false;
+#else
     constexpr bool SUSP = (GEO || ONE) && !REL && !XA;
+#endif
     const uint32_t susp_end = GEO ? L.qd : L.qsl;
 
     if (lane == 0) {
@@ -665,34 +669,11 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
 
         // ---- best-first loop (iteration 0 scores the entry point) --------------
         QVG_PH(long long ph_issue = 0, ph_wait = 0, ph_dist = 0, ph_merge = 0, ph_pick = 0, ph_tma = 0;)
+        for (;;) {  // (re-entered only when a hand-over finds the FIFO full)
         for (;;) {
             QVG_PH(long long tp0 = clock64();)
             if constexpr (SUSP) {
-                if (__builtin_expect(budget_left == 0, 0)) {
-                    // end of this unit: save the state and hand the query to the FIFO
-                    // (a full FIFO just lets this warp finish the query)
-                    uint32_t slot = 0;
-                    if (lane == 0) slot = atomicAdd(a.susp_ctl, 1u);
-                    slot = __shfl_sync(kFull, slot, 0);
-                    if (slot < a.susp_cap) {
-                        uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
-                        const uint32_t blob16 = (susp_end - L.pk) / 16u;
-                        const uint4* src = reinterpret_cast<const uint4*>(base + L.pk);
-                        for (uint32_t i = lane; i < blob16; i += 32) __stcg(sstate + 4 + i, src[i]);
-                        for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
-                        if (lane == 0) {
-                            __stcg(sstate, make_uint4(np, tn, tdist, hint));
-                            __stcg(sstate + 1, make_uint4(n, c_exp, c_tie, c_eval));
-                            __stcg(sstate + 2, make_uint4(c_drop, c_slots, c_maxtie, overflow ? 1u : 0u));
-                        }
-                        __threadfence();
-                        __syncwarp();
-                        if (lane == 0)
-                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.susp_list + slot), "r"((uint32_t)q + 1u) : "memory");
-                        break;
-                    }
-                    budget_left = kNoBudget;
-                }
+                if (__builtin_expect(budget_left == 0, 0)) break;  // end of this unit (below)
             }
             c_eval += n;
             // (a) TMA-gather the code rows (double-buffered halves of SR rows)
@@ -1193,6 +1174,33 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 if (keep[j]) cid[pos++] = v[j];
             __syncwarp();
             QVG_PH(ph_pick += clock64() - tp3;)
+        }
+        if (!(SUSP && budget_left == 0)) break;  // the search ended
+        // end of a unit (the loop stopped at the top of an iteration): save the
+        // state and hand the query to the FIFO; a full FIFO lets this warp finish it
+        {
+            uint32_t slot = 0;
+            if (lane == 0) slot = atomicAdd(a.susp_ctl, 1u);
+            slot = __shfl_sync(kFull, slot, 0);
+            if (slot < a.susp_cap) {
+                uint4* sstate = a.susp_state + (size_t)(q - a.susp_from) * a.susp_stride16;
+                const uint32_t blob16 = (susp_end - L.pk) / 16u;
+                const uint4* src = reinterpret_cast<const uint4*>(base + L.pk);
+                for (uint32_t i = lane; i < blob16; i += 32) __stcg(sstate + 4 + i, src[i]);
+                for (int off = 16; off > 0; off >>= 1) c_drop += __shfl_xor_sync(kFull, c_drop, off);
+                if (lane == 0) {
+                    __stcg(sstate, make_uint4(np, tn, tdist, hint));
+                    __stcg(sstate + 1, make_uint4(n, c_exp, c_tie, c_eval));
+                    __stcg(sstate + 2, make_uint4(c_drop, c_slots, c_maxtie, overflow ? 1u : 0u));
+                }
+                __threadfence();
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.susp_list + slot), "r"((uint32_t)q + 1u) : "memory");
+                break;
+            }
+            budget_left = kNoBudget;
+        }
         }
 
         if (SUSP && budget_left == 0) continue;
