@@ -344,9 +344,10 @@ qvg_status run(qvg_index* h, const float* queries, const uint64_t* qcodes, uint6
         }();
         const uint64_t wpb = pinfo.warps_per_block ? pinfo.warps_per_block : kWarpsPerBlock;
         const uint64_t slots = grid * wpb;
-        // (ef < 32: a query is ~50 us, a hand-off ~3 us: whole queries win, ef 16 -1.7 %)
+        // (small ef: a query is 50-100 us, a hand-off ~3 us, whole queries win:
+        // ef 16 -1.7 % on cfg 2, ef 32 0 % on cfg 2 and -5 % on its clustered variant)
         if (susp_env && pinfo.susp_blob_bytes && !exact && !relax && !xa && h->has_tmap &&
-            ef >= 32 && nq > slots && nq < (1ull << 31)) {
+            ef >= 48 && nq > slots && nq < (1ull << 31)) {
             // the last round's queries (one per warp slot) run in units of about a
             // quarter of a query
             const uint64_t nb = nq < slots ? nq : slots;

@@ -220,7 +220,7 @@ def test_pinned_result_buffers_with_tie_spill_rerun():
 
 # ------------------------------------------------ tail balancing (suspended queries)
 @pytest.mark.gpu
-@pytest.mark.parametrize("ef", [32, 64, 130])
+@pytest.mark.parametrize("ef", [48, 64, 130])
 def test_tail_balancing_units_resume_exactly(ef):
     """Batches larger than one round of warp slots on the headline geometry
     (D = 768, R = 64) run their last round in units: a warp saves the query's
