@@ -1,7 +1,7 @@
 # same-box A/B of bench.py lines with parity: bash tools/ab.sh "ARGS" LIB1 LIB2 ...  (TOOL)
 ARGS=$1; shift
 for L in "$@"; do
-  QVG_LIB=$L timeout 600 python bench.py $ARGS --no-cpu-baseline --recall-queries 0 --relaxed none > /tmp/ab.json 2>/tmp/ab.err || tail -3 /tmp/ab.err
+  QVG_LIB=$L timeout 600 python bench.py $ARGS --no-cpu-baseline --recall-queries 0 --relaxed none --variant-rows none > /tmp/ab.json 2>/tmp/ab.err || tail -3 /tmp/ab.err
   python - "$L" <<'P'
 import json, sys
 d = json.load(open('/tmp/ab.json'))
