@@ -942,7 +942,38 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 const bool few = mu <= 8u;
                 if (few && lane >= mu && lane < 8u) csrp[lane] = 0xFFFFFFFFu;
                 __syncwarp();
-                if (lo < np) {
+                // two 32-entry chunks per round (both read before either is
+                // written: entries only move right), half the warp barriers: ef 256
+                // 8.53 -> 8.34 ms, ef 128 +0.7 %, ef 64 unchanged.  Not in the
+                // fused-prologue instantiations: there its mere presence cost 0.5 %
+                // at ef 64 (profiles/r3_merge2_ab.txt)
+                if (!PRO && lo < np && few) {
+                    const uint4 r0 = reinterpret_cast<const uint4*>(csrp)[0];
+                    const uint4 r1 = reinterpret_cast<const uint4*>(csrp)[1];
+                    auto dest = [&](uint32_t idx) {
+                        return idx + (r0.x <= idx) + (r0.y <= idx) + (r0.z <= idx) + (r0.w <= idx) +
+                               (r1.x <= idx) + (r1.y <= idx) + (r1.z <= idx) + (r1.w <= idx);
+                    };
+                    for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 64) {
+                        const uint32_t ia = (uint32_t)cb + lane;
+                        const uint32_t ib = ia - 32u;  // (wraps below chunk 0: then >= np)
+                        const bool ma = ia < np && ia >= lo, mb = ib < np && ib >= lo;
+                        uint64_t pa = 0, pb = 0;
+                        if (ma) pa = pk[ia];
+                        if (mb) pb = pk[ib];
+                        const uint32_t na2 = dest(ia), nb2 = dest(ib);
+                        __syncwarp();
+                        if (ma) {
+                            if (na2 < ef) pk[na2] = pa;
+                            else if (!REL) evk[na2 - ef] = pa;
+                        }
+                        if (mb) {
+                            if (nb2 < ef) pk[nb2] = pb;
+                            else if (!REL) evk[nb2 - ef] = pb;
+                        }
+                        __syncwarp();
+                    }
+                } else if (lo < np) {
                     for (int cb = (int)((np - 1) & ~31u); cb >= (int)(lo & ~31u); cb -= 32) {
                         const uint32_t idx = (uint32_t)cb + lane;
                         const bool mv = idx < np && idx >= lo;
