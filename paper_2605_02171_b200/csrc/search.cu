@@ -856,7 +856,13 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                     uint32_t d = 0;
                     if (valid) {
                         const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
-                        d = row_sm2(qc, rowp, W, rot, part, LPR);
+                        // (cfg 3 3.95 -> 3.80 ms, cfg 4 7.13 -> 6.86 ms: profiles/r3_smfix_*)
+                        if constexpr (WC == 24 || WC == 48) {
+                            if (LPR == (uint32_t)(WC / 12)) d = row_sm2_fixed<WC, WC / 12>(qc, rowp, lane);
+                            else d = row_sm2(qc, rowp, W, rot, part, LPR);
+                        } else {
+                            d = row_sm2(qc, rowp, W, rot, part, LPR);
+                        }
                     }
                     for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
                     const bool lead = valid && part == 0;

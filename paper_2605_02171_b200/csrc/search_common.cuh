@@ -118,6 +118,34 @@ __device__ __forceinline__ uint32_t row_sm2(const uint4* __restrict__ qc,
     return acc.total();
 }
 
+// The same with the code width WC and the lanes per row L as compile-time
+// constants (wide rows: WC = 24 with L = 2, WC = 48 with L = 4; rows start on
+// the same bank quad, 16·WC being a multiple of 128 B).  Lane (row r, part p)
+// starts at chunk s = L·(r mod 8/L) + p <= 7 and steps by L: the 8 lanes of an
+// LDS.128 phase (8/L rows x L parts) hit 8 distinct bank quads, and the first
+// (WC - 8)/L + 1 chunks of every lane need no wrap — constant offsets from two
+// base pointers instead of per-chunk index arithmetic.
+template <int WC, int L>
+__device__ __forceinline__ uint32_t row_sm2_fixed(const uint4* __restrict__ qc,
+                                                  const uint4* __restrict__ row, uint32_t lane) {
+    static_assert(WC % L == 0 && 8 % L == 0 && (16 * WC) % 128 == 0, "geometry");
+    constexpr int N = WC / L;             // chunks per lane
+    constexpr int NF = (WC - 8) / L + 1;  // of which wrap-free for every start <= 7
+    const uint32_t s = L * ((lane / L) & (8 / L - 1)) + (lane & (L - 1));
+    const uint4* q = qc + s;
+    const uint4* r = row + s;
+    Sm2Acc acc;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) acc.add(q[L * i], r[L * i]);
+#pragma unroll
+    for (int i = NF; i < N; ++i) {
+        uint32_t c = s + (uint32_t)(L * i);
+        c = c >= (uint32_t)WC ? c - WC : c;
+        acc.add(qc[c], row[c]);
+    }
+    return acc.total();
+}
+
 // first index i in [0, n) with ordk(a[i]) >= x.  4-ary: three independent
 // pivot loads per round, half the dependent shared-memory round trips of a
 // binary search (cfg 2 ef 256: 10.16 -> 10.13 ms; with the merge's broadcast
