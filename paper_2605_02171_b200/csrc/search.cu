@@ -837,6 +837,18 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                                 cc = cc >= (uint32_t)WC ? cc - WC : cc;
                                 acc.add(qc[cc], rowp[cc]);
                             }
+                        } else if constexpr (WC == 6) {
+                            // 96-B rows: row r starts on bank quad 6r mod 8 = {0,6,4,2} x 2,
+                            // so starting rows r and r + 4 of an LDS.128 phase one chunk
+                            // apart puts the 8 lanes on 8 distinct quads; five chunks of
+                            // every lane need no wrap
+                            const uint32_t r1 = (lane >> 2) & 1u;
+                            const uint4* qr = qc + r1;
+                            const uint4* rr = rowp + r1;
+#pragma unroll
+                            for (int c = 0; c < 5; ++c) acc.add(qr[c], rr[c]);
+                            const uint32_t cl = r1 ? 0u : 5u;
+                            acc.add(qc[cl], rowp[cl]);
                         } else {
                             uint32_t cc = rot;
 #pragma unroll 4
@@ -951,9 +963,10 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                 // two 32-entry chunks per round (both read before either is
                 // written: entries only move right), half the warp barriers: ef 256
                 // 8.53 -> 8.34 ms, ef 128 +0.7 %, ef 64 unchanged.  Not in the
-                // fused-prologue instantiations: there its mere presence cost 0.5 %
-                // at ef 64 (profiles/r3_merge2_ab.txt)
-                if (!PRO && lo < np && few) {
+                // fused-prologue instantiations (there its mere presence cost 0.5 %
+                // at ef 64, profiles/r3_merge2_ab.txt) nor in the R = 32 kernels
+                // (cfg 1 -3.5 %, profiles/r3_w6_ab.txt)
+                if ((GEO || ONE) && !PRO && lo < np && few) {
                     const uint4 r0 = reinterpret_cast<const uint4*>(csrp)[0];
                     const uint4 r1 = reinterpret_cast<const uint4*>(csrp)[1];
                     auto dest = [&](uint32_t idx) {
