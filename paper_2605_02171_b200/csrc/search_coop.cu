@@ -274,7 +274,10 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                         uint32_t d = 0;
                         if (j < cnt) {
                             const uint4* rowp = st + ((j >> 2) * gstride + (j & 3u) * rowb) / 16u;
-                            d = row_sm2(qc, rowp, W, rot, part, LPR);
+                            // (wide rows: compile-time code width and lanes per row)
+                            if (W == 24u && LPR == 2u) d = row_sm2_fixed<24, 2>(qc, rowp, lane);
+                            else if (W == 48u && LPR == 2u) d = row_sm2_fixed<48, 2>(qc, rowp, lane);
+                            else d = row_sm2(qc, rowp, W, rot, part, LPR);
                         }
                         for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
                         const bool lead = j < cnt && part == 0;
