@@ -146,6 +146,31 @@ __device__ __forceinline__ uint32_t row_sm2_fixed(const uint4* __restrict__ qc,
     return acc.total();
 }
 
+// The same for rows that alternate between two bank-quad bases (16·WC is an odd
+// multiple of 64 B, e.g. WC = 12): two adjacent rows cover all 8 quads once they
+// share a start chunk, so the rotation advances by L per PAIR of rows; start
+// chunks are <= 3 and the first (WC - 4)/L + 1 chunks of every lane are wrap-free.
+template <int WC, int L>
+__device__ __forceinline__ uint32_t row_sm2_fixed_alt(const uint4* __restrict__ qc,
+                                                      const uint4* __restrict__ row, uint32_t lane) {
+    static_assert(WC % L == 0 && 4 % L == 0 && (16 * WC) % 128 == 64, "geometry");
+    constexpr int N = WC / L;
+    constexpr int NF = (WC - 4) / L + 1;
+    const uint32_t s = L * ((lane / (2 * L)) & (4 / L - 1)) + (lane & (L - 1));
+    const uint4* q = qc + s;
+    const uint4* r = row + s;
+    Sm2Acc acc;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) acc.add(q[L * i], r[L * i]);
+#pragma unroll
+    for (int i = NF; i < N; ++i) {
+        uint32_t c = s + (uint32_t)(L * i);
+        c = c >= (uint32_t)WC ? c - WC : c;
+        acc.add(qc[c], row[c]);
+    }
+    return acc.total();
+}
+
 // first index i in [0, n) with ordk(a[i]) >= x.  4-ary: three independent
 // pivot loads per round, half the dependent shared-memory round trips of a
 // binary search (cfg 2 ef 256: 10.16 -> 10.13 ms; with the merge's broadcast

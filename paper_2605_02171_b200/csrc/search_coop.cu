@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kCoopWarps * 32) coop_kernel(
                             // (wide rows: compile-time code width and lanes per row)
                             if (W == 24u && LPR == 2u) d = row_sm2_fixed<24, 2>(qc, rowp, lane);
                             else if (W == 48u && LPR == 2u) d = row_sm2_fixed<48, 2>(qc, rowp, lane);
+                            else if (W == 12u && LPR == 2u) d = row_sm2_fixed_alt<12, 2>(qc, rowp, lane);
                             else d = row_sm2(qc, rowp, W, rot, part, LPR);
                         }
                         for (uint32_t o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(kFull, d, o);
