@@ -1389,7 +1389,26 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                         }
                         __syncwarp();
                         const double2* q2 = reinterpret_cast<const double2*>(qd);
-                        if (row < NR) {
+                        if ((ONE || PRO) && row < NR && lim == 4u * kMaxSL4 && i0 + 4u * kMaxSL4 <= main4) {
+                            // a full 48-float slice of 4-element groups (every slice when
+                            // D is a multiple of 48): no per-group bounds checks.  cfg 3
+                            // 3.79 -> 3.61 ms, cfg 1 e2e +2.5 %; left out of the R = 32
+                            // device-query kernels, where it measured -0.7 %
+                            // (profiles/r4_rrfull_*_ab.txt)
+                            const float4* rp = reinterpret_cast<const float4*>(
+                                stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
+#pragma unroll
+                            for (uint32_t u = 0; u < kMaxSL4; ++u) {
+                                const float4 v = rp[u];
+                                const double2 qa = q2[2 * u], qb = q2[2 * u + 1];
+                                s0 = __fma_rn(qa.x, (double)v.x, s0);
+                                s1 = __fma_rn(qa.y, (double)v.y, s1);
+                                s2 = __fma_rn(qb.x, (double)v.z, s2);
+                                s3 = __fma_rn(qb.y, (double)v.w, s3);
+                            }
+                            if (s == nsl - 1)
+                                sc[row] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                        } else if (row < NR) {
                             const float4* rp = reinterpret_cast<const float4*>(
                                 stage0 + h * stage_delta + (lane >> 2) * cgs + (lane & 3u) * SL * 4u);
 #pragma unroll
