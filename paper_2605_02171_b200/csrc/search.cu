@@ -1297,7 +1297,11 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
             // rerank: one lane per pool entry, 4 sequential double chains
             const float* qv = a.qn + q * ix.Dp;
             __syncwarp();
-            if (LEAN || SL) {
+            // (R = 32 / W = 6 geometry, D <= 384: the rows are short and mostly in L2;
+            // one lane streaming each row measured 4.6 % faster than the TMA slices
+            // (e2e +8.7 %): profiles/r5_cfg1_ldg_rerank.txt, r5_ldg6_ab.txt)
+            constexpr bool kLdgRerank = WC == 6;
+            if (!kLdgRerank && (LEAN || SL)) {
                 // TMA column slices: round t stages slice (t % nsl) of the 32 pool
                 // rows of group (t / nsl) — 4 rows x SL floats per gather4 —
                 // into a stage half; lane r owns row 32g + r and advances its 4
