@@ -1440,6 +1440,43 @@ __global__ void __launch_bounds__((GEO || ONE) ? kGeoMaxWarps * 32 : kWarpsPerBl
                     }
                     if (t + 2 < rounds) rr_issue(t + 2);
                 }
+            } else if (kLdgRerank && (ix.dim % 48u) == 0u) {
+                // one lane per pool entry streaming its row from global, 48 elements
+                // at a time; the query chunk is converted to doubles once per warp
+                // (two conversions per lane) and read back by 16-B broadcast loads
+                for (uint32_t idx = lane; idx < NR; idx += 32)
+                    prefetch_l2(ix.cold + (size_t)(uint32_t)pk[idx] * ix.Dp, ix.Dp * 4u);
+                const double2* q2 = reinterpret_cast<const double2*>(qd);
+                for (uint32_t g0 = 0; g0 < NR; g0 += 32) {
+                    const uint32_t idx = g0 + lane;
+                    const float4* r4 = reinterpret_cast<const float4*>(
+                        ix.cold + (size_t)(uint32_t)pk[idx < NR ? idx : g0] * ix.Dp);
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                    for (uint32_t c0 = 0; c0 < ix.dim; c0 += 48) {
+                        __syncwarp();  // the previous chunk's doubles are consumed
+                        if (lane < 24) {
+                            const float2 f = __ldg(reinterpret_cast<const float2*>(qv + c0) + lane);
+                            reinterpret_cast<double2*>(qd)[lane] = make_double2((double)f.x, (double)f.y);
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int hb = 0; hb < 2; ++hb) {
+                            float4 b[6];
+#pragma unroll
+                            for (int u = 0; u < 6; ++u) b[u] = __ldg(r4 + c0 / 4 + hb * 6 + u);
+#pragma unroll
+                            for (int u = 0; u < 6; ++u) {
+                                const double2 qa = q2[2 * (hb * 6 + u)], qb = q2[2 * (hb * 6 + u) + 1];
+                                s0 = __fma_rn(qa.x, (double)b[u].x, s0);
+                                s1 = __fma_rn(qa.y, (double)b[u].y, s1);
+                                s2 = __fma_rn(qb.x, (double)b[u].z, s2);
+                                s3 = __fma_rn(qb.y, (double)b[u].w, s3);
+                            }
+                        }
+                    }
+                    if (idx < NR)
+                        sc[idx] = __double2float_rn(__dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3)));
+                }
             } else {
                 // fallback: one lane per pool entry streaming its row from global
                 if (!(a.variant & 1u))
